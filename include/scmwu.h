@@ -1,0 +1,136 @@
+/*
+ * scmwu.h — C ABI of the B200-native SCMWU feasibility-test engine.
+ *
+ * Drop-in boundary for the reference's hot path (R = /root/reference/pkg/src/symcone/):
+ *
+ *   sc_create       replaces the per-solve setup in solve_ses / solve_svm
+ *                   (R/ses.py:147-169, R/svm.py:164-187): the instance is copied to HBM
+ *                   once; the OracleSpec factory's constants (cone, width rho,
+ *                   trace bound R, rank) become handle properties.
+ *   sc_ftp          replaces ONE call of meta.solve_ftp (R/meta.py:244-395) or
+ *                   meta.refine_run (R/meta.py:457-573) — the whole iteration loop,
+ *                   including every Scmwu.current/observe (R/mwu.py:57-70), oracle
+ *                   query (R/ses.py:90-132, R/svm.py:97-127), progress evaluation
+ *                   (R/ses.py:82-87, R/svm.py:87-94) and pd_counter (R/svm.py:173-181),
+ *                   runs inside one persistent kernel launch.
+ *   sc_progress     replaces ses_progress / svm_progress at a host-given point
+ *                   (seed certificates R/ses.py:174-176, R/svm.py:194-199 and the final
+ *                   enclosure slack R/ses.py:187).
+ *   sc_iterate      materialises the trace-one iterate p of the last sc_ftp call
+ *                   (PrimalCertificate.p / DualFeasible.p_last, R/meta.py:123,132).
+ *   sc_pd_commit /  keep the best polytope-distance pair across calls and materialise
+ *   sc_pd_pair      it (best_pd in R/svm.py:171-181, read at :229-231).
+ *
+ * Conventions: plain pointers and sizes, caller-owned host buffers are only read
+ * (or written) during the call, all device memory is owned by the handle, one
+ * handle = one thread of control (R/mwu.py:41-43).  Status codes:
+ */
+#ifndef SCMWU_H
+#define SCMWU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sc_status {
+    SC_OK = 0,
+    SC_EARG = 1,       /* bad argument (ValueError in the reference) */
+    SC_ECUDA = 2,      /* CUDA runtime error / no device */
+    SC_ENCCL = 3,      /* cross-GPU exchange error */
+    SC_EWIDTH = 4,     /* witness residual exceeded the width: WidthViolationError */
+    SC_EOOM = 5,       /* device allocation failed */
+    SC_ETRACE = 6      /* non-positive trace while normalising (ValueError, R/cones.py:417) */
+};
+
+enum sc_kind { SC_SES = 0, SC_SVM = 1 };
+enum sc_mode { SC_MODE_FTP = 0, SC_MODE_REFINE = 1 };
+enum sc_result_kind { SC_PRIMAL = 0, SC_DUAL = 1 };
+enum sc_reason {
+    SC_REASON_SEPARATED = 0,
+    SC_REASON_EXHAUSTED = 1,
+    SC_REASON_EARLY_STOP = 2,
+    SC_REASON_AFFIRMATIVE = 3,
+    SC_REASON_REFINED = 4
+};
+
+typedef struct sc_handle sc_handle;
+
+/* Problem constants, computed by the caller exactly as the reference does. */
+typedef struct {
+    int32_t kind;      /* SC_SES or SC_SVM */
+    int32_t d;         /* point dimension */
+    int64_t n;         /* number of points (SES) / n1 + n2 (SVM) */
+    int64_t n1;        /* SVM: the first n1 rows are P, the rest Q; SES: ignored */
+    double D;          /* SES: ses_range D (R/ses.py:65-72); SVM: max_norm (R/svm.py:62-66) */
+    double rho;        /* width: 3D/sqrt2 (R/ses.py:161) or 2D (R/svm.py:168) */
+    double R;          /* trace bound: sqrt2 (R/ses.py:169) or 2 (R/svm.py:186) */
+    int64_t rank;      /* cone rank: 2(n-1) (SES) or n (SVM) (R/cones.py:72-74) */
+    double ln_r;       /* math.log(rank) evaluated on the host (bit-exact with Python) */
+    int32_t grid;      /* CTAs of the persistent kernel (0 = auto) */
+    int32_t device;    /* CUDA device ordinal */
+} sc_problem;
+
+/* One feasibility test. */
+typedef struct {
+    int32_t mode;          /* SC_MODE_FTP or SC_MODE_REFINE */
+    int32_t has_progress;  /* FTP: progress callback present (always 1 in the solvers) */
+    double alpha;          /* level */
+    double eps;            /* FTP: requested tolerance */
+    int64_t budget;        /* FTP: min(iteration_bound, cap) (R/meta.py:282-284); REFINE: unused */
+    int64_t horizon;       /* REFINE: max(horizon, ceil(ln r)) (R/meta.py:479) */
+    int64_t ceil_ln_r;     /* math.ceil(ln r) */
+    double delta;          /* EarlyStopConfig.delta */
+    int32_t patience;      /* EarlyStopConfig.patience */
+    int32_t enabled;       /* EarlyStopConfig.enabled */
+    double gain_rel;       /* REFINE: gain_rel (already defaulted to delta) */
+    double lo, hi;         /* REFINE: bracket bounds (-inf/+inf when absent) */
+    double target;         /* REFINE: target relative width; NaN = none */
+} sc_ftp_args;
+
+/* Outcome of one feasibility test.  Vector outputs are written to caller
+ * buffers of dual_dim = d+1 (SES) or d+2 (SVM) doubles. */
+typedef struct {
+    int32_t kind;          /* SC_PRIMAL or SC_DUAL */
+    int32_t reason;        /* enum sc_reason */
+    int64_t iterations;
+    double eps_eff;        /* DUAL */
+    double value;          /* DUAL: certified claim value */
+    double oracle_value;   /* PRIMAL: the negative oracle value */
+    int32_t has_best_f, has_best_counter, has_claim_y;
+    double best_f, best_counter;
+    /* width violation (status SC_EWIDTH) */
+    int64_t width_iteration;
+    double width_norm;
+    /* SVM polytope-distance bookkeeping (R/svm.py:173-181, :201-204) */
+    int32_t has_counter_min;  /* a pd_counter evaluation happened in this call */
+    double counter_min;       /* smallest distance seen in this call (strict <) */
+    double sep_dist;          /* PRIMAL: |P^T mu - Q^T gam| of the separating iterate */
+    /* device-side timing and work accounting of this call */
+    int64_t passes;           /* streaming passes over X executed */
+    float kernel_ms;          /* CUDA-event time of the persistent kernel */
+} sc_ftp_result;
+
+/* X: row-major host rows.  SES: n rows (centres), radii n values.  SVM: the n1
+ * rows of P; X_tail (if not NULL) holds the n - n1 rows of Q, otherwise X
+ * holds all n rows; radii must be NULL. */
+int sc_create(const sc_problem* prob, const double* X, const double* X_tail,
+              const double* radii, sc_handle** out);
+int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
+           double* y_tilde /* dual_dim */, double* best_y /* dual_dim */);
+int sc_progress(sc_handle* h, const double* y /* d values */, double* f);
+int sc_iterate(sc_handle* h, double* p /* SES (n-1)(d+1), SVM n */);
+int sc_pd_commit(sc_handle* h, int32_t which /* 0: call minimum, 1: separating iterate */);
+int sc_pd_pair(sc_handle* h, double* mu /* n1 */, double* gam /* n - n1 */, double* dist);
+int sc_set_grid(sc_handle* h, int32_t grid);
+int sc_info(const sc_handle* h, int64_t* out /* 8 values: grid, threads, lanes_per_row,
+              cols_per_lane, tile_rows, stages, resident, smem_bytes */);
+const char* sc_last_error(const sc_handle* h);
+void sc_destroy(sc_handle* h);
+int sc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCMWU_H */

@@ -1,0 +1,232 @@
+"""ctypes binding of the C ABI in include/scmwu.h.
+
+The product loads ``libscmwu.so`` (built in-tree by ``build.py`` / ``__graft_entry__.build()``)
+from this package directory.  There is no CPU fallback: if the library is
+missing, or reports that no CUDA device is usable, the solvers raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from typing import Optional
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_NAME = "libscmwu.so"
+
+SC_OK, SC_EARG, SC_ECUDA, SC_ENCCL, SC_EWIDTH, SC_EOOM, SC_ETRACE = range(7)
+SC_SES, SC_SVM = 0, 1
+SC_MODE_FTP, SC_MODE_REFINE = 0, 1
+SC_PRIMAL, SC_DUAL = 0, 1
+REASONS = {0: "separated", 1: "exhausted", 2: "early_stop", 3: "affirmative", 4: "refined"}
+
+INT64_MAX = (1 << 63) - 1
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA engine library is missing or cannot run here."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"scmwu status {status}: {msg}")
+
+
+class ScProblem(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("d", ctypes.c_int32), ("n", ctypes.c_int64),
+                ("n1", ctypes.c_int64), ("D", ctypes.c_double), ("rho", ctypes.c_double),
+                ("R", ctypes.c_double), ("rank", ctypes.c_int64), ("ln_r", ctypes.c_double),
+                ("grid", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class ScFtpArgs(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("has_progress", ctypes.c_int32),
+                ("alpha", ctypes.c_double), ("eps", ctypes.c_double),
+                ("budget", ctypes.c_int64), ("horizon", ctypes.c_int64),
+                ("ceil_ln_r", ctypes.c_int64), ("delta", ctypes.c_double),
+                ("patience", ctypes.c_int32), ("enabled", ctypes.c_int32),
+                ("gain_rel", ctypes.c_double), ("lo", ctypes.c_double),
+                ("hi", ctypes.c_double), ("target", ctypes.c_double)]
+
+
+class ScFtpResult(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("reason", ctypes.c_int32),
+                ("iterations", ctypes.c_int64), ("eps_eff", ctypes.c_double),
+                ("value", ctypes.c_double), ("oracle_value", ctypes.c_double),
+                ("has_best_f", ctypes.c_int32), ("has_best_counter", ctypes.c_int32),
+                ("has_claim_y", ctypes.c_int32), ("best_f", ctypes.c_double),
+                ("best_counter", ctypes.c_double), ("width_iteration", ctypes.c_int64),
+                ("width_norm", ctypes.c_double), ("has_counter_min", ctypes.c_int32),
+                ("counter_min", ctypes.c_double), ("sep_dist", ctypes.c_double),
+                ("passes", ctypes.c_int64), ("kernel_ms", ctypes.c_float)]
+
+
+EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "sc_pd_pair",
+           "sc_set_grid", "sc_info", "sc_last_error", "sc_destroy", "sc_version")
+
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+def _ptr(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_dp)
+
+
+class Engine:
+    """One loaded implementation of the C ABI."""
+
+    def __init__(self, path: str):
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} is missing: build it with `python build.py` "
+                f"(nvcc, sm_100a); there is no CPU fallback")
+        self.path = path
+        lib = ctypes.CDLL(path)
+        vp = ctypes.c_void_p
+        lib.sc_create.argtypes = [ctypes.POINTER(ScProblem), _dp, _dp, _dp, ctypes.POINTER(vp)]
+        lib.sc_ftp.argtypes = [vp, ctypes.POINTER(ScFtpArgs), ctypes.POINTER(ScFtpResult), _dp,
+                               _dp]
+        lib.sc_progress.argtypes = [vp, _dp, _dp]
+        lib.sc_iterate.argtypes = [vp, _dp]
+        lib.sc_pd_commit.argtypes = [vp, ctypes.c_int32]
+        lib.sc_pd_pair.argtypes = [vp, _dp, _dp, _dp]
+        lib.sc_set_grid.argtypes = [vp, ctypes.c_int32]
+        lib.sc_info.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
+        lib.sc_last_error.argtypes = [vp]
+        lib.sc_last_error.restype = ctypes.c_char_p
+        lib.sc_destroy.argtypes = [vp]
+        lib.sc_destroy.restype = None
+        lib.sc_version.restype = ctypes.c_int
+        self.lib = lib
+
+    def create(self, kind: int, X, X_tail, radii, D: float, rho: float, R: float,
+               rank: int, n1: int = 0, grid: int = 0, device: int = 0) -> "Handle":
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        Xt = None if X_tail is None else np.ascontiguousarray(X_tail, dtype=np.float64)
+        rad = None if radii is None else np.ascontiguousarray(radii, dtype=np.float64)
+        n = X.shape[0] + (0 if Xt is None else Xt.shape[0])
+        d = X.shape[1]
+        prob = ScProblem(kind=kind, d=d, n=n, n1=n1, D=D, rho=rho, R=R, rank=rank,
+                         ln_r=math.log(rank), grid=grid, device=device)
+        h = ctypes.c_void_p()
+        st = self.lib.sc_create(ctypes.byref(prob), _ptr(X), _ptr(Xt), _ptr(rad),
+                                ctypes.byref(h))
+        if st != SC_OK:
+            msg = self.lib.sc_last_error(h).decode() if h.value else "sc_create failed"
+            if st == SC_ECUDA:
+                raise NativeUnavailable(f"CUDA engine cannot run: {msg}")
+            raise NativeError(st, msg)
+        return Handle(self, h, prob)
+
+
+class FtpOut:
+    """Plain view of one sc_ftp call."""
+
+    __slots__ = ("status", "kind", "reason", "iterations", "eps_eff", "value", "oracle_value",
+                 "best_f", "best_counter", "y_tilde", "best_y", "width_iteration",
+                 "width_norm", "counter_min", "sep_dist", "passes", "kernel_ms", "has_claim_y")
+
+
+class Handle:
+    def __init__(self, engine: Engine, h: ctypes.c_void_p, prob: ScProblem):
+        self.engine = engine
+        self.h = h
+        self.prob = prob
+        self.d = prob.d
+        self.dual_dim = prob.d + (1 if prob.kind == SC_SES else 2)
+        self.calls = 0
+
+    def _check(self, st: int, what: str):
+        if st != SC_OK:
+            raise NativeError(st, f"{what}: {self.engine.lib.sc_last_error(self.h).decode()}")
+
+    def ftp(self, args: ScFtpArgs) -> FtpOut:
+        res = ScFtpResult()
+        yt = np.zeros(self.dual_dim)
+        by = np.zeros(self.dual_dim)
+        st = self.engine.lib.sc_ftp(self.h, ctypes.byref(args), ctypes.byref(res), _ptr(yt),
+                                    _ptr(by))
+        self.calls += 1
+        if st not in (SC_OK, SC_EWIDTH):
+            self._check(st, "sc_ftp")
+        o = FtpOut()
+        o.status = st
+        o.kind = res.kind
+        o.reason = REASONS.get(res.reason, "?")
+        o.iterations = int(res.iterations)
+        o.eps_eff = res.eps_eff
+        o.value = res.value
+        o.oracle_value = res.oracle_value
+        o.best_f = res.best_f if res.has_best_f else None
+        o.best_counter = res.best_counter if res.has_best_counter else None
+        o.y_tilde = yt
+        o.best_y = by if res.has_best_f else None
+        o.has_claim_y = bool(res.has_claim_y)
+        o.width_iteration = int(res.width_iteration)
+        o.width_norm = res.width_norm
+        o.counter_min = res.counter_min if res.has_counter_min else None
+        o.sep_dist = res.sep_dist
+        o.passes = int(res.passes)
+        o.kernel_ms = float(res.kernel_ms)
+        return o
+
+    def progress(self, y) -> float:
+        y = np.ascontiguousarray(np.asarray(y, dtype=np.float64)[: self.d])
+        f = ctypes.c_double()
+        self._check(self.engine.lib.sc_progress(self.h, _ptr(y), ctypes.byref(f)), "sc_progress")
+        return float(f.value)
+
+    def iterate(self) -> np.ndarray:
+        n, d = self.prob.n, self.prob.d
+        size = (n - 1) * (d + 1) if self.prob.kind == SC_SES else n
+        out = np.empty(size)
+        self._check(self.engine.lib.sc_iterate(self.h, _ptr(out)), "sc_iterate")
+        return out
+
+    def pd_commit(self, which: int) -> None:
+        self._check(self.engine.lib.sc_pd_commit(self.h, which), "sc_pd_commit")
+
+    def pd_pair(self):
+        n1 = self.prob.n1
+        mu = np.empty(n1)
+        gam = np.empty(self.prob.n - n1)
+        dist = ctypes.c_double()
+        self._check(self.engine.lib.sc_pd_pair(self.h, _ptr(mu), _ptr(gam), ctypes.byref(dist)),
+                    "sc_pd_pair")
+        return mu, gam, float(dist.value)
+
+    def set_grid(self, grid: int) -> None:
+        self._check(self.engine.lib.sc_set_grid(self.h, grid), "sc_set_grid")
+
+    def info(self) -> dict:
+        out = (ctypes.c_int64 * 8)()
+        self._check(self.engine.lib.sc_info(self.h, out), "sc_info")
+        keys = ("grid", "threads", "lanes_per_row", "cols_per_lane", "tile_rows", "stages",
+                "resident", "smem_bytes")
+        return dict(zip(keys, [int(v) for v in out]))
+
+    def close(self) -> None:
+        if self.h is not None and self.h.value:
+            self.engine.lib.sc_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+_cuda_engine: Optional[Engine] = None
+
+
+def cuda_engine() -> Engine:
+    """The B200 engine (paper_2405_09157_b200/libscmwu.so).  Raises if absent."""
+    global _cuda_engine
+    if _cuda_engine is None:
+        _cuda_engine = Engine(os.path.join(PKG_DIR, LIB_NAME))
+    return _cuda_engine

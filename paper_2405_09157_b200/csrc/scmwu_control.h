@@ -1,0 +1,592 @@
+// scmwu_control.h — the per-iteration control of one feasibility test, run
+// on the device between streaming passes (the "K3 tail" of DESIGN.md).
+//
+// It restates, with the deferred-check schedule of DESIGN.md §4, the loop
+// bodies of meta.solve_ftp (R/meta.py:294-395) and meta.refine_run
+// (R/meta.py:499-573), the oracle epilogues of ses_oracle (R/ses.py:101-132)
+// and svm_oracle (R/svm.py:101-127), and the bookkeeping of _ProgressState
+// (R/meta.py:398-429), _dual_feasible (R/meta.py:436-446) and pd_counter
+// (R/svm.py:173-181).  R = /root/reference/pkg/src/symcone/.
+//
+// Pass k (one stream over X) reduces, from the state after iteration k-1:
+//   * the oracle sums of iterate k (closed form of the cumulative loss, so the
+//     learner state is O(d): DESIGN.md §3), and
+//   * every check of iteration k-1 (width, progress of the averages, window
+//     average, SVM candidate margin and counter candidate).
+// after_pass() then finishes iteration k-1 in reference order and, unless
+// that terminates the test, runs iterate k's separation test and update.
+//
+// Every lane of the executing warp runs this code redundantly on private
+// scalars; the O(d) vectors live in shared memory and are partitioned by
+// index (element j is owned by lane j % nl), so no intra-warp hazards exist.
+// The same header compiles for the host (tests/emu), with one lane.
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/scmwu.h"
+
+#if defined(__CUDACC__)
+#define SC_HD __host__ __device__ __forceinline__
+#else
+#define SC_HD inline
+#endif
+
+namespace scmwu {
+
+// control constants, verbatim (R/meta.py:238-241, :449-454, R/mwu.py:23)
+constexpr int kLadderBase = 64;
+constexpr int kLadderFactor = 8;
+constexpr int kCheckEvery = 16;
+constexpr int kProgressStride = 4;
+constexpr double kValueTrendDrop = 0.05;
+constexpr double kLossSlack = 1e-9;
+constexpr double kSqrt2 = 1.4142135623730951;
+
+// ---- layout of one reduced pass vector ------------------------------------
+// SES: T, Lin, Rad, M (max lambda+), F (max progress of U/t), Wd (max residual
+//      eigen-magnitude of iteration t), Fw (max progress of the window avg),
+//      then Sd[d] = sum_i c_i (U - t v_i).
+// SVM: TP, TQ, M (max logit), minresP, minresQ, Wd (max |res|), minPW, maxQW,
+//      minPy, maxQy, minPz, maxQz, then GP[d], GQ[d].
+enum SesRed { kS_T = 0, kS_Lin, kS_Rad, kS_M, kS_F, kS_Wd, kS_Fw, kS_Vec };
+enum SvmRed { kV_TP = 0, kV_TQ, kV_M, kV_minresP, kV_minresQ, kV_Wd, kV_minPW, kV_maxQW,
+              kV_minPy, kV_maxQy, kV_minPz, kV_maxQz, kV_Vec };
+
+SC_HD int red_width(int kind, int d) { return kind == SC_SES ? kS_Vec + d : kV_Vec + 2 * d; }
+// per-CTA partial layout: SES identical to the reduced one; SVM carries one side
+// (T, M, minres, Wd, extW, extY, extZ, G[d]) — the side is known from the CTA index.
+enum SvmPart { kP_T = 0, kP_M, kP_minres, kP_Wd, kP_extW, kP_extY, kP_extZ, kP_Vec };
+SC_HD int part_width(int kind, int d) { return kind == SC_SES ? kS_Vec + d : kP_Vec + d; }
+
+// Parameters the next streaming pass reads (written by lane 0 of the control warp).
+struct PassParams {
+    double t;          // learner step count of the state (iteration k-1)
+    double alpha;
+    double eta_rho;    // eta / rho
+    double shift;      // lagged exponent shift
+    double S1, S2;     // SVM: sums of s1, s2
+    double s1p, s2p;   // SVM: s1, s2 of iteration k-1
+    int check;         // iteration k-1 is a check iteration (window / counter)
+    int action;        // 0 = pass, 1 = done
+};
+
+// Device-memory slots describing an iterate, so p can be rebuilt on demand.
+struct IterState {
+    double t, eta, shift, T, TP, TQ, S1, S2;
+};
+
+enum Action { kPass = 0, kDone = 1 };
+enum Flow { kContinue = 0, kBreak = 1, kStop = 2 };
+
+// Shared-memory vector workspace of the control (all of length >= dd).
+struct CtlVecs {
+    double* ysum;    // y_sum (U or W in its first d entries)
+    double* yprev;   // y of iteration k-1 (u or w, then alpha or s1,s2)
+    double* wsum;    // window_sum
+    double* besty;   // _ProgressState.best_y
+    double* claimy;  // best_claim_y (FTP)
+    double* ywin;    // window average of the last check iteration
+    double* zv;      // SVM: P^T mu^ - Q^T gam^ of the last check iteration
+    double* ynew;    // scratch: y of the iterate being processed
+    double* pU;      // state vector (y_sum before update) of the latest iterate
+    double* v1;      // SES: anchor centre
+};
+
+// Global-memory slots (device) written by the CTA whose `writer` flag is set.
+struct CtlSlots {
+    double* ring;        // window history, ring_cap x dd
+    int64_t ring_cap;
+    double* pd_pending;  // SVM: iterate state at the last check  [d+2 | IterState]
+    double* pd_callmin;  // SVM: state at the call's smallest counter distance
+    double* pd_sep;      // SVM: state of the separating iterate
+    double* last;        // state of the latest iterate (for sc_iterate)
+};
+
+template <class L>
+struct Control {
+    // ---------------- problem (constant)
+    int kind, d, dd;
+    bool is_max;
+    double rho, inv_rho, R, ln_r, D, g1;
+    // ---------------- call arguments
+    sc_ftp_args a;
+    // ---------------- learner / rung state
+    int64_t t, T;            // step count, horizon of the rung / run
+    int64_t budget, spent, rung_T, remaining;
+    int rung_index;
+    double eta;
+    int64_t win_head, win_count, win_len;  // ring indices (monotone) and live length
+    // FTP early-stop state
+    bool has_f_prev; double f_prev; int streak; bool early;
+    bool has_f_start; double f_start;
+    double f_last;           // progress of the last finished iteration (FTP)
+    // REFINE state
+    int64_t stall_floor, last_gain;
+    bool has_anchor; double anchor;
+    bool has_val_anchor; double val_anchor;
+    double lo, hi;
+    // best / claims
+    bool has_best_f; double best_f;
+    bool has_best_counter; double best_counter;
+    double claim_eps; bool has_claim;
+    // deferred data of iteration t (the latest accepted iterate)
+    double value_prev;       // oracle value of iteration t
+    double dist_prev;        // SVM counter distance of iteration t (if check)
+    bool check_prev;
+    // SVM pd bookkeeping
+    bool has_counter_min; double counter_min;
+    // latest iterate state (for p)
+    IterState cur;           // state of the iterate being processed
+    double shift_pass;       // shift used by the pass that produced `red`
+    // results
+    sc_ftp_result* res;      // written by all lanes identically; copied out by the writer
+    int status;
+    bool writer;
+
+    CtlVecs v;
+    CtlSlots s;
+
+    // ------------------------------------------------------------ helpers
+    SC_HD bool is_check(int64_t tt) const {
+        return tt % kCheckEvery == 0 || tt == T || tt == 1;
+    }
+    SC_HD bool is_prog(int64_t tt) const {
+        return tt % kProgressStride == 0 || tt == 1 || tt == T;
+    }
+    SC_HD bool better(double f) const {
+        return !has_best_f || (is_max ? f < best_f : f > best_f);
+    }
+    // offer(f, y_sum / t)
+    SC_HD void offer_bar(double f) {
+        if (!better(f)) return;
+        has_best_f = true; best_f = f;
+        const double tt = (double)t;
+        for (int j = L::lane(); j < dd; j += L::nl()) v.besty[j] = v.ysum[j] / tt;
+    }
+    SC_HD void offer_vec(double f, const double* y) {
+        if (!better(f)) return;
+        has_best_f = true; best_f = f;
+        for (int j = L::lane(); j < dd; j += L::nl()) v.besty[j] = y[j];
+    }
+    // offer(progress(z), (z; 0; 0))  — SVM counter candidate (R/svm.py:181, R/meta.py:348-349)
+    SC_HD void offer_z(double f) {
+        if (!better(f)) return;
+        has_best_f = true; best_f = f;
+        for (int j = L::lane(); j < dd; j += L::nl()) v.besty[j] = j < d ? v.zv[j] : 0.0;
+    }
+    SC_HD void offer_counter(double cv) {
+        if (!has_best_counter || (is_max ? cv > best_counter : cv < best_counter)) {
+            has_best_counter = true; best_counter = cv;
+        }
+    }
+    SC_HD bool beats(double alpha) const {
+        return has_best_f && (is_max ? best_f < alpha : best_f > alpha);
+    }
+    SC_HD double claim_value(double e) const {
+        return is_max ? (1.0 + e) * a.alpha : (1.0 - e) * a.alpha;
+    }
+    // SVM certified margin of direction w with extremes (minP, maxQ) and norm nrm
+    // (R/svm.py:87-94)
+    static SC_HD double svm_margin(double minP, double maxQ, double nrm) {
+        if (nrm == 0.0) return 0.0;
+        double sep = (minP - maxQ) / nrm;
+        return sep > 0.0 ? sep : 0.0;
+    }
+    SC_HD double norm_d(const double* x) const {
+        double acc = 0.0;
+        for (int j = L::lane(); j < d; j += L::nl()) acc += x[j] * x[j];
+        return sqrt(L::sum(acc));
+    }
+    SC_HD void save_state(double* slot, const double* vec, const IterState& st) {
+        if (!writer) return;
+        for (int j = L::lane(); j < dd; j += L::nl()) slot[j] = vec[j];
+        if (L::lane() == 0) *reinterpret_cast<IterState*>(slot + dd + (dd & 1)) = st;
+    }
+    SC_HD void copy_slot(double* dst, const double* src) {
+        if (!writer) return;
+        const int w = dd + (dd & 1) + (int)(sizeof(IterState) / sizeof(double));
+        for (int j = L::lane(); j < w; j += L::nl()) dst[j] = L::ldcg(src + j);
+    }
+
+    // ------------------------------------------------------------ results
+    SC_HD int finish_primal(double value, int64_t iters) {
+        res->kind = SC_PRIMAL; res->reason = SC_REASON_SEPARATED;
+        res->iterations = iters; res->oracle_value = value;
+        return finish_common();
+    }
+    // _dual_feasible (R/meta.py:436-446); y_bar from `src` (already divided) or
+    // y_sum / t when src == nullptr and use_sum.
+    SC_HD int finish_dual(int reason, int64_t iters, double eps_eff, double value,
+                          const double* src, bool have_y, bool from_sum, double* y_tilde) {
+        res->kind = SC_DUAL; res->reason = reason; res->iterations = iters;
+        double e = eps_eff;
+        if (!have_y) e = INFINITY;
+        res->eps_eff = e; res->value = value; res->has_claim_y = have_y ? 1 : 0;
+        const double sh = (e < 1.0 ? e : 1.0) * a.alpha / R;
+        for (int j = L::lane(); j < dd; j += L::nl()) {
+            double y = !have_y ? 0.0 : from_sum ? v.ysum[j] / (double)t : src[j];
+            if (j == dd - 1) y += is_max ? sh : -sh;
+            y_tilde[j] = y;
+        }
+        return finish_common();
+    }
+    SC_HD int finish_common() {
+        res->has_best_f = has_best_f; res->best_f = has_best_f ? best_f : 0.0;
+        res->has_best_counter = has_best_counter;
+        res->best_counter = has_best_counter ? best_counter : 0.0;
+        res->has_counter_min = has_counter_min;
+        res->counter_min = has_counter_min ? counter_min : 0.0;
+        status = SC_OK;
+        save_state(s.last, v.pU, cur);
+        return kDone;
+    }
+
+    // ------------------------------------------------------------ call start
+    // red0: the reduced vector of iterate 1 (all logits zero), precomputed.
+    SC_HD int begin(const sc_ftp_args& args, const double* red0, double* y_tilde,
+                    double* best_y_out, PassParams* pp) {
+        a = args;
+        has_best_f = false; best_f = 0.0; has_best_counter = false; best_counter = 0.0;
+        has_counter_min = false; counter_min = 0.0;
+        claim_eps = INFINITY; has_claim = false;
+        spent = 0; rung_index = 0; status = SC_OK;
+        res->sep_dist = 0.0; res->width_iteration = 0; res->width_norm = 0.0;
+        if (a.mode == SC_MODE_FTP) {
+            budget = a.budget;
+            int64_t base = kLadderBase > a.ceil_ln_r ? kLadderBase : a.ceil_ln_r;
+            rung_T = budget < base ? budget : base;
+            return start_rung(red0, y_tilde, pp);
+        }
+        // refine_run (R/meta.py:474-497)
+        T = a.horizon;
+        eta = sqrt(ln_r / (double)T);
+        int64_t sf = (int64_t)ceil(16.0 / eta);
+        stall_floor = 64 * (int64_t)a.patience > sf ? 64 * (int64_t)a.patience : sf;
+        has_anchor = false; has_val_anchor = false; last_gain = 0;
+        lo = a.lo; hi = a.hi;
+        reset_learner();
+        return process_iterate(red0, y_tilde, pp);
+    }
+
+    SC_HD void reset_learner() {
+        t = 0; win_head = 0; win_count = 0; win_len = 0;
+        for (int j = L::lane(); j < dd; j += L::nl()) { v.ysum[j] = 0.0; v.wsum[j] = 0.0; }
+        shift_pass = 0.0;
+    }
+
+    SC_HD int final_exhausted(double* y_tilde) {
+        int64_t it = spent > 1 ? spent : 1;
+        return finish_dual(SC_REASON_EXHAUSTED, it, claim_eps, claim_value(claim_eps), v.claimy,
+                           has_claim, false, y_tilde);
+    }
+
+    // top of `while spent < budget` (R/meta.py:294-311)
+    SC_HD int start_rung(const double* red0, double* y_tilde, PassParams* pp) {
+        if (!(spent < budget)) return final_exhausted(y_tilde);
+        remaining = budget - spent;
+        if ((double)remaining < ln_r) return final_exhausted(y_tilde);
+        if (remaining < rung_T) rung_T = remaining;
+        T = rung_T;
+        eta = sqrt(ln_r / (double)rung_T);
+        has_f_prev = false; f_prev = 0.0; streak = 0; early = false;
+        has_f_start = has_best_f; f_start = best_f;
+        reset_learner();
+        return process_iterate(red0, y_tilde, pp);
+    }
+
+    // ------------------------------------------------------------ iterate k = t+1
+    SC_HD int process_iterate(const double* red, double* y_tilde, PassParams* pp) {
+        const int64_t k = t + 1;
+        const int nl = L::nl(), ln = L::lane();
+        double value;
+        cur.t = (double)t; cur.eta = eta; cur.shift = shift_pass;
+        for (int j = ln; j < dd; j += nl) v.pU[j] = v.ysum[j];
+        if (kind == SC_SES) {
+            // s = sum_i W_i = -(eta/rho)/T * sum_i c_i (U - t v_i)      (R/ses.py:109-112)
+            const double Tt = red[kS_T];
+            cur.T = Tt;
+            if (a.alpha < g1) {          // R/ses.py:103-105
+                return finish_sep(-INFINITY, k, red, y_tilde);
+            }
+            const double coef = -(eta * inv_rho) / Tt;
+            double s2 = 0.0;
+            for (int j = ln; j < d; j += nl) {
+                double sj = coef * red[kS_Vec + j];
+                v.ynew[j] = sj;          // temporarily s
+                s2 += sj * sj;
+            }
+            const double sn = sqrt(L::sum(s2));
+            double su = 0.0;
+            for (int j = ln; j < d; j += nl) {
+                double sj = v.ynew[j];
+                double u = sn > 0.0 ? v.v1[j] + (a.alpha - g1) * (sj / sn) : v.v1[j];
+                su += sj * u;
+                v.ynew[j] = u;
+            }
+            su = L::sum(su);
+            const double lin = coef * red[kS_Lin];
+            const double rad = red[kS_Rad] / (kSqrt2 * Tt);
+            value = su + a.alpha / kSqrt2 - lin - rad;            // R/ses.py:123
+            if (value < 0.0) return finish_sep(value, k, red, y_tilde);
+            for (int j = ln; j < dd; j += nl)
+                if (j == d) v.ynew[j] = a.alpha;                 // y = (u; alpha)
+        } else {
+            // g = P^T mu - Q^T gam with mu = e/T                  (R/svm.py:104-119)
+            const double TP = red[kV_TP], TQ = red[kV_TQ];
+            const double Tt = TP + TQ;
+            cur.T = Tt; cur.TP = TP; cur.TQ = TQ;
+            cur.S1 = v.ysum[d]; cur.S2 = v.ysum[d + 1];
+            double g2 = 0.0;
+            for (int j = ln; j < d; j += nl) {
+                double gj = (red[kV_Vec + j] - red[kV_Vec + d + j]) / Tt;
+                v.ynew[j] = gj;
+                g2 += gj * gj;
+            }
+            const double gn = sqrt(L::sum(g2));
+            double gw = 0.0;
+            for (int j = ln; j < d; j += nl) {
+                double gj = v.ynew[j];
+                double w = gn > 0.0 ? gj / gn : (j == 0 ? 1.0 : 0.0);
+                gw += gj * w;
+                v.ynew[j] = w;
+            }
+            gw = L::sum(gw);
+            const double tm = TP / Tt, tg = TQ / Tt;
+            const double s1 = tm <= tg ? D : a.alpha - D;
+            const double s2v = a.alpha - s1;
+            value = gw - tm * s1 - tg * s2v;                      // R/svm.py:118
+            if (value < 0.0) return finish_sep(value, k, red, y_tilde);
+            for (int j = ln; j < dd; j += nl) {                  // y = (w; s1; s2)
+                if (j == d) v.ynew[j] = s1;
+                if (j == d + 1) v.ynew[j] = s2v;
+            }
+        }
+        L::sync();
+        // ---- accepted witness: y_sum += y; the width check is deferred to the next pass
+        const bool chk = is_check(k);
+        if (kind == SC_SVM && chk) {
+            // pd_counter at this iterate (R/svm.py:173-181): z = GP/TP - GQ/TQ
+            const double TP = red[kV_TP], TQ = red[kV_TQ];
+            double z2 = 0.0;
+            for (int j = ln; j < d; j += nl) {
+                double z = red[kV_Vec + j] / TP - red[kV_Vec + d + j] / TQ;
+                v.zv[j] = z;
+                z2 += z * z;
+            }
+            dist_prev = sqrt(L::sum(z2));
+            save_state(s.pd_pending, v.pU, cur);
+        }
+        for (int j = ln; j < dd; j += nl) {
+            double y = v.ynew[j];
+            v.ysum[j] += y;
+            v.yprev[j] = y;
+        }
+        t = k;
+        value_prev = value;
+        check_prev = chk;
+        push_window(k);
+        if (chk) {
+            const double len = (double)win_len;
+            for (int j = ln; j < dd; j += nl) v.ywin[j] = v.wsum[j] / len;
+        }
+        // lagged shift for the next pass: the max eigenvalue / logit of this iterate
+        const double m = kind == SC_SES ? red[kS_M] : red[kV_M];
+        shift_pass = m;
+        L::sync();
+        write_pass(pp);
+        return kPass;
+    }
+
+    SC_HD int finish_sep(double value, int64_t k, const double* red, double* y_tilde) {
+        if (kind == SC_SVM) {
+            const double TP = red[kV_TP], TQ = red[kV_TQ];
+            double z2 = 0.0;
+            for (int j = L::lane(); j < d; j += L::nl()) {
+                double z = red[kV_Vec + j] / TP - red[kV_Vec + d + j] / TQ;
+                z2 += z * z;
+            }
+            res->sep_dist = sqrt(L::sum(z2));
+            save_state(s.pd_sep, v.pU, cur);
+        }
+        const int64_t iters = a.mode == SC_MODE_FTP ? spent + k : k;
+        return finish_primal(value, iters);
+    }
+
+    // suffix window (R/meta.py:330-335 / :514-519)
+    SC_HD void push_window(int64_t tt) {
+        const int nl = L::nl(), ln = L::lane();
+        double* slot = s.ring + (win_count % s.ring_cap) * dd;
+        for (int j = ln; j < dd; j += nl) {
+            double y = v.ynew[j];
+            if (writer) slot[j] = y;
+            v.wsum[j] += y;
+        }
+        ++win_count; ++win_len;
+        const int64_t lim = kLadderBase > tt / 2 ? kLadderBase : tt / 2;
+        while (win_len > lim) {
+            const double* old = s.ring + (win_head % s.ring_cap) * dd;
+            for (int j = ln; j < dd; j += nl) v.wsum[j] -= L::ldcg(old + j);
+            ++win_head; --win_len;
+        }
+    }
+
+    SC_HD void write_pass(PassParams* pp) {
+        if (L::lane() != 0) return;
+        pp->t = (double)t;
+        pp->alpha = a.alpha;
+        pp->eta_rho = eta * inv_rho;
+        pp->shift = shift_pass;
+        pp->check = check_prev ? 1 : 0;
+        if (kind == SC_SVM) {
+            pp->S1 = v.ysum[d]; pp->S2 = v.ysum[d + 1];
+            pp->s1p = v.yprev[d]; pp->s2p = v.yprev[d + 1];
+        }
+        pp->action = kPass;
+    }
+
+    // ------------------------------------------------------------ after a pass
+    // `red` reduces iterate t+1 (speculative) and the checks of iteration t.
+    SC_HD int after_pass(const double* red, const double* red0, double* y_tilde,
+                         PassParams* pp) {
+        int flow = finish_iteration(red, y_tilde);
+        if (flow == kStop) return kDone;
+        if (flow == kContinue && t < T) return process_iterate(red, y_tilde, pp);
+        // end of the rung (FTP) or of the run (REFINE)
+        if (a.mode == SC_MODE_REFINE) {
+            const double tt = (double)t;
+            const double e = R * rho * (eta + ln_r / (eta * tt)) / a.alpha;  // R/meta.py:570
+            return finish_dual(SC_REASON_REFINED, t, e, claim_value(e), nullptr, true, true,
+                               y_tilde);
+        }
+        return end_rung(red0, y_tilde, pp);
+    }
+
+    // R/meta.py:366-389
+    SC_HD int end_rung(const double* red0, double* y_tilde, PassParams* pp) {
+        spent += t;
+        const double tt = (double)t;
+        const double e_here = R * rho * (eta + ln_r / (eta * tt)) / a.alpha;
+        if (e_here < claim_eps) {
+            claim_eps = e_here; has_claim = true;
+            for (int j = L::lane(); j < dd; j += L::nl()) v.claimy[j] = v.ysum[j] / tt;
+        }
+        if (claim_eps <= a.eps)
+            return finish_dual(SC_REASON_EXHAUSTED, spent, claim_eps, claim_value(claim_eps),
+                               v.claimy, has_claim, false, y_tilde);
+        if (early && rung_index >= 1 && a.has_progress) {
+            bool stalled = has_f_start && has_best_f &&
+                           fabs(f_start - best_f) <= a.delta * fabs(f_start);
+            if (stalled)
+                return finish_dual(SC_REASON_EARLY_STOP, spent, claim_eps,
+                                   claim_value(claim_eps), v.claimy, has_claim, false, y_tilde);
+        }
+        rung_index += 1;
+        int64_t nxt = rung_T * kLadderFactor;
+        rung_T = remaining < nxt ? remaining : nxt;
+        return start_rung(red0, y_tilde, pp);
+    }
+
+    // Finish iteration t (its observe + progress bookkeeping), reference order
+    // R/meta.py:323-364 (FTP) / :509-568 (REFINE).
+    SC_HD int finish_iteration(const double* red, double* y_tilde) {
+        const bool ftp = a.mode == SC_MODE_FTP;
+        // Scmwu.observe width check (R/mwu.py:62-64) -> WidthViolationError
+        const double wd = kind == SC_SES ? red[kS_Wd] : red[kV_Wd];
+        const double nrm = wd * inv_rho;
+        if (nrm > 1.0 + kLossSlack) {
+            res->width_iteration = ftp ? spent + t : t;
+            res->width_norm = nrm * rho;
+            finish_common();
+            status = SC_EWIDTH;
+            return kStop;
+        }
+        if (ftp && !a.has_progress) return kContinue;
+        const double tt = (double)t;
+        // per-witness candidate (SVM, R/svm.py:123-127) offered with y
+        if (kind == SC_SVM) {
+            double mw = (red[kV_minresP] + red[kV_minresQ]) + a.alpha;
+            offer_vec(mw > 0.0 ? mw : 0.0, v.yprev);
+        }
+        // progress of the running average
+        double f;
+        if (kind == SC_SES) {
+            f = red[kS_F];
+        } else {
+            f = svm_margin(red[kV_minPW], red[kV_maxQW], norm_d(v.ysum));
+        }
+        if (ftp || is_prog(t)) offer_bar(f);
+        if (check_prev) {
+            double fw = kind == SC_SES ? red[kS_Fw]
+                                        : svm_margin(red[kV_minPy], red[kV_maxQy], norm_d(v.ywin));
+            offer_vec(fw, v.ywin);
+            if (kind == SC_SVM) {
+                const double cv = dist_prev;
+                if (!has_counter_min || cv < counter_min) {
+                    has_counter_min = true; counter_min = cv;
+                    copy_slot(s.pd_callmin, s.pd_pending);
+                }
+                offer_counter(cv);
+                offer_z(svm_margin(red[kV_minPz], red[kV_maxQz], cv));
+            }
+        }
+        L::sync();
+        if (ftp) {
+            if (beats(a.alpha)) {
+                finish_dual(SC_REASON_AFFIRMATIVE, spent + t, 0.0, best_f, v.besty, true, false,
+                            y_tilde);
+                return kStop;
+            }
+            if (a.enabled) {
+                if (has_f_prev && f_prev != 0.0) {
+                    if (fabs(f - f_prev) / fabs(f_prev) < a.delta) {
+                        streak += 1;
+                        if (streak >= a.patience) { early = true; return kBreak; }
+                    } else {
+                        streak = 0;
+                    }
+                }
+                has_f_prev = true; f_prev = f;
+            }
+            return kContinue;
+        }
+        // refine stall rule (R/meta.py:537-555)
+        bool gained = false;
+        if (!has_anchor || (has_best_f && fabs(best_f - anchor) > a.gain_rel * fabs(anchor))) {
+            // anchor = state.best_f (may be None)
+            has_anchor = has_best_f; anchor = best_f;   // anchor = state.best_f (None stays None)
+            gained = true;
+        }
+        {
+            const double vv = value_prev;
+            if (!has_val_anchor) {
+                has_val_anchor = true; val_anchor = vv;
+            } else if (vv < val_anchor - kValueTrendDrop * fabs(val_anchor)) {
+                val_anchor = vv; gained = true;
+            }
+        }
+        if (gained) {
+            last_gain = t;
+        } else if (a.enabled) {
+            int64_t lim = stall_floor > t / 3 ? stall_floor : t / 3;
+            if (t - last_gain > lim) return kBreak;
+        }
+        if (!isnan(a.target) && t % kProgressStride == 0) {
+            if (has_best_f) {
+                if (is_max) hi = hi < best_f ? hi : best_f;
+                else lo = lo > best_f ? lo : best_f;
+            }
+            if (has_best_counter) {
+                if (is_max) lo = lo > best_counter ? lo : best_counter;
+                else hi = hi < best_counter ? hi : best_counter;
+            }
+            const double lp = lo > 0.0 ? lo : 0.0;
+            if (hi - lo <= a.target * lp) return kBreak;
+        }
+        (void)tt;
+        return kContinue;
+    }
+};
+
+}  // namespace scmwu

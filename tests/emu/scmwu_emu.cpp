@@ -1,0 +1,303 @@
+// scmwu_emu.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A single-threaded host emulation of the CUDA engine: the same control
+// header (paper_2405_09157_b200/csrc/scmwu_control.h) driven by a plain C++
+// loop that computes the streaming pass row by row with the same closed-form
+// formulas as the CUDA kernel.  It exports the sc_* C ABI of include/scmwu.h
+// so the host layer can be exercised on a machine without a GPU
+// (tests/test_emu_*.py).  It is never loaded by the product package.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../paper_2405_09157_b200/csrc/scmwu_control.h"
+
+using namespace scmwu;
+
+namespace {
+
+struct HostLanes {
+    static int lane() { return 0; }
+    static int nl() { return 1; }
+    static double sum(double x) { return x; }
+    static void sync() {}
+    static double ldcg(const double* p) { return *p; }
+};
+
+constexpr double kInvSqrt2 = 0.7071067811865476;
+
+}  // namespace
+
+struct sc_handle {
+    sc_problem prob;
+    int dd;
+    std::vector<double> X, radii;       // n x d, n
+    std::vector<double> red0;
+    std::vector<double> ring, pd_pending, pd_callmin, pd_sep, pd_best, last;
+    std::string err;
+};
+
+static int fail(sc_handle* h, int code, const char* msg) {
+    if (h) h->err = msg;
+    return code;
+}
+
+static int slot_len(int dd) { return dd + (dd & 1) + (int)(sizeof(IterState) / sizeof(double)); }
+
+static void pass_ses(const sc_handle* h, const PassParams& pp, const double* U,
+                     const double* up, const double* yw, double* red) {
+    const int d = h->prob.d;
+    const int64_t n = h->prob.n;
+    double T = 0, Lin = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
+    std::vector<double> Sd(d, 0.0), df(d);
+    const double t = pp.t, er = pp.eta_rho, al = pp.alpha;
+    for (int64_t i = 0; i < n; ++i) {
+        const double* v = &h->X[i * d];
+        const double g = h->radii[i];
+        double a = 0, l = 0, w2 = 0, f2 = 0;
+        for (int j = 0; j < d; ++j) {
+            double x = fma(-t, v[j], U[j]);
+            df[j] = x;
+            a = fma(x, x, a);
+            l = fma(v[j], x, l);
+            double w = up[j] - v[j];
+            w2 = fma(w, w, w2);
+            if (pp.check) { double y = yw[j] - v[j]; f2 = fma(y, y, f2); }
+        }
+        const double ra = sqrt(a);
+        F = fmax(F, ra / t + g);
+        if (pp.check) Fw = fmax(Fw, sqrt(f2) + g);
+        if (i == 0) continue;
+        const double nrm = er * ra;
+        const double x0 = -er * (t * (al - g));
+        const double lp = (x0 + nrm) * kInvSqrt2, lm = (x0 - nrm) * kInvSqrt2;
+        const double A = exp(lp - pp.shift), B = exp(lm - pp.shift);
+        const double c = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
+        T += A + B;
+        Lin = fma(c, l, Lin);
+        Rad = fma(g, A + B, Rad);
+        M = fmax(M, lp);
+        Wd = fmax(Wd, (fabs(al - g) + sqrt(w2)) * kInvSqrt2);
+        for (int j = 0; j < d; ++j) Sd[j] = fma(c, df[j], Sd[j]);
+    }
+    red[kS_T] = T; red[kS_Lin] = Lin; red[kS_Rad] = Rad; red[kS_M] = M;
+    red[kS_F] = F; red[kS_Wd] = Wd; red[kS_Fw] = Fw;
+    for (int j = 0; j < d; ++j) red[kS_Vec + j] = Sd[j];
+}
+
+static void pass_svm(const sc_handle* h, const PassParams& pp, const double* W,
+                     const double* wp, const double* yw, const double* z, double* red) {
+    const int d = h->prob.d;
+    const int64_t n = h->prob.n, n1 = h->prob.n1;
+    double TP = 0, TQ = 0, M = -INFINITY, mrP = INFINITY, mrQ = INFINITY, Wd = 0;
+    double mPW = INFINITY, xQW = -INFINITY, mPy = INFINITY, xQy = -INFINITY;
+    double mPz = INFINITY, xQz = -INFINITY;
+    std::vector<double> GP(d, 0.0), GQ(d, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        const double* x = &h->X[i * d];
+        const bool P = i < n1;
+        double dW = 0, dw = 0, dy = 0, dz = 0;
+        for (int j = 0; j < d; ++j) {
+            dW = fma(x[j], W[j], dW);
+            dw = fma(x[j], wp[j], dw);
+            if (pp.check) { dy = fma(x[j], yw[j], dy); dz = fma(x[j], z[j], dz); }
+        }
+        const double sg = P ? 1.0 : -1.0;
+        const double lg = -pp.eta_rho * (sg * dW - (P ? pp.S1 : pp.S2));
+        const double e = exp(lg - pp.shift);
+        M = fmax(M, lg);
+        const double r = sg * dw - (P ? pp.s1p : pp.s2p);
+        Wd = fmax(Wd, fabs(r));
+        std::vector<double>& G = P ? GP : GQ;
+        if (P) {
+            TP += e; mrP = fmin(mrP, r); mPW = fmin(mPW, dW);
+            if (pp.check) { mPy = fmin(mPy, dy); mPz = fmin(mPz, dz); }
+        } else {
+            TQ += e; mrQ = fmin(mrQ, r); xQW = fmax(xQW, dW);
+            if (pp.check) { xQy = fmax(xQy, dy); xQz = fmax(xQz, dz); }
+        }
+        for (int j = 0; j < d; ++j) G[j] = fma(e, x[j], G[j]);
+    }
+    red[kV_TP] = TP; red[kV_TQ] = TQ; red[kV_M] = M; red[kV_minresP] = mrP;
+    red[kV_minresQ] = mrQ; red[kV_Wd] = Wd; red[kV_minPW] = mPW; red[kV_maxQW] = xQW;
+    red[kV_minPy] = mPy; red[kV_maxQy] = xQy; red[kV_minPz] = mPz; red[kV_maxQz] = xQz;
+    for (int j = 0; j < d; ++j) { red[kV_Vec + j] = GP[j]; red[kV_Vec + d + j] = GQ[j]; }
+}
+
+extern "C" {
+
+int sc_version(void) { return 1000; }
+
+int sc_create(const sc_problem* prob, const double* X, const double* X_tail,
+              const double* radii, sc_handle** out) {
+    if (!prob || !X || !out) return SC_EARG;
+    if (prob->d < 1 || prob->n < 2) return SC_EARG;
+    if (prob->kind == SC_SES && !radii) return SC_EARG;
+    if (prob->kind == SC_SVM && (prob->n1 < 1 || prob->n1 >= prob->n)) return SC_EARG;
+    sc_handle* h = new sc_handle();
+    h->prob = *prob;
+    const int d = prob->d;
+    const int64_t n = prob->n;
+    h->dd = prob->kind == SC_SES ? d + 1 : d + 2;
+    if (X_tail) {
+        h->X.assign(X, X + prob->n1 * d);
+        h->X.insert(h->X.end(), X_tail, X_tail + (n - prob->n1) * d);
+    } else {
+        h->X.assign(X, X + n * d);
+    }
+    if (prob->kind == SC_SES) h->radii.assign(radii, radii + n);
+    h->red0.assign(red_width(prob->kind, d), 0.0);
+    if (prob->kind == SC_SES) {
+        double rad = 0;
+        for (int64_t i = 1; i < n; ++i) rad += 2.0 * h->radii[i];
+        h->red0[kS_T] = 2.0 * (double)(n - 1);
+        h->red0[kS_Rad] = rad;
+        h->red0[kS_M] = 0.0;
+    } else {
+        h->red0[kV_TP] = (double)prob->n1;
+        h->red0[kV_TQ] = (double)(n - prob->n1);
+        for (int64_t i = 0; i < n; ++i)
+            for (int j = 0; j < d; ++j)
+                h->red0[kV_Vec + (i < prob->n1 ? 0 : d) + j] += h->X[i * d + j];
+    }
+    const int sl = slot_len(h->dd);
+    h->pd_pending.assign(sl, 0.0);
+    h->pd_callmin.assign(sl, 0.0);
+    h->pd_sep.assign(sl, 0.0);
+    h->pd_best.assign(sl, 0.0);   // t = 0 state == uniform weights
+    h->last.assign(sl, 0.0);
+    *out = h;
+    return SC_OK;
+}
+
+int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_tilde,
+           double* best_y) {
+    if (!h || !args || !res || !y_tilde || !best_y) return SC_EARG;
+    memset(res, 0, sizeof(*res));
+    const int d = h->prob.d, dd = h->dd;
+    const int64_t T = args->mode == SC_MODE_FTP ? args->budget : args->horizon;
+    if (T < 1) return fail(h, SC_EARG, "budget/horizon must be >= 1");
+    // the ring holds at most max(64, T_rung/2)+1 live entries; the largest rung is <= T
+    int64_t cap = (T / 2 > kLadderBase ? T / 2 : kLadderBase) + 2;
+    if (args->mode == SC_MODE_FTP && cap > (1 << 24)) cap = (1 << 24);
+    h->ring.assign((size_t)cap * dd, 0.0);
+
+    std::vector<double> ysum(dd), yprev(dd), wsum(dd), besty(dd), claimy(dd), ywin(dd),
+        zv(dd), ynew(dd), pU(dd), v1(dd, 0.0);
+    if (h->prob.kind == SC_SES)
+        for (int j = 0; j < d; ++j) v1[j] = h->X[j];
+    Control<HostLanes> c;
+    c.kind = h->prob.kind; c.d = d; c.dd = dd;
+    c.is_max = h->prob.kind == SC_SES;
+    c.rho = h->prob.rho; c.inv_rho = 1.0 / h->prob.rho; c.R = h->prob.R;
+    c.ln_r = h->prob.ln_r; c.D = h->prob.D;
+    c.g1 = h->prob.kind == SC_SES ? h->radii[0] : 0.0;
+    c.res = res; c.writer = true;
+    c.v = CtlVecs{ysum.data(), yprev.data(), wsum.data(), besty.data(), claimy.data(),
+                  ywin.data(), zv.data(), ynew.data(), pU.data(), v1.data()};
+    c.s = CtlSlots{h->ring.data(), cap, h->pd_pending.data(), h->pd_callmin.data(),
+                   h->pd_sep.data(), h->last.data()};
+    PassParams pp{};
+    std::vector<double> red(red_width(h->prob.kind, d));
+    int act = c.begin(*args, h->red0.data(), y_tilde, best_y, &pp);
+    int64_t passes = 0;
+    while (act == kPass) {
+        if (h->prob.kind == SC_SES)
+            pass_ses(h, pp, ysum.data(), yprev.data(), ywin.data(), red.data());
+        else
+            pass_svm(h, pp, ysum.data(), yprev.data(), ywin.data(), zv.data(), red.data());
+        ++passes;
+        act = c.after_pass(red.data(), h->red0.data(), y_tilde, &pp);
+    }
+    for (int j = 0; j < dd; ++j) best_y[j] = besty[j];
+    res->passes = passes;
+    if (c.status == SC_EWIDTH) return fail(h, SC_EWIDTH, "width violation");
+    return c.status;
+}
+
+int sc_progress(sc_handle* h, const double* y, double* f) {
+    if (!h || !y || !f) return SC_EARG;
+    const int d = h->prob.d;
+    const int64_t n = h->prob.n;
+    if (h->prob.kind == SC_SES) {
+        double best = -INFINITY;
+        for (int64_t i = 0; i < n; ++i) {
+            double s = 0;
+            for (int j = 0; j < d; ++j) { double x = h->X[i * d + j] - y[j]; s = fma(x, x, s); }
+            best = fmax(best, sqrt(s) + h->radii[i]);
+        }
+        *f = best;
+    } else {
+        double nrm = 0, mP = INFINITY, xQ = -INFINITY;
+        for (int j = 0; j < d; ++j) nrm += y[j] * y[j];
+        nrm = sqrt(nrm);
+        for (int64_t i = 0; i < n; ++i) {
+            double s = 0;
+            for (int j = 0; j < d; ++j) s = fma(h->X[i * d + j], y[j], s);
+            if (i < h->prob.n1) mP = fmin(mP, s); else xQ = fmax(xQ, s);
+        }
+        *f = Control<HostLanes>::svm_margin(mP, xQ, nrm);
+    }
+    return SC_OK;
+}
+
+int sc_pd_commit(sc_handle* h, int32_t which) {
+    if (!h || h->prob.kind != SC_SVM) return SC_EARG;
+    if (which == 0) h->pd_best = h->pd_callmin;
+    else if (which == 1) h->pd_best = h->pd_sep;
+    else return SC_EARG;
+    return SC_OK;
+}
+
+int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
+    if (!h || h->prob.kind != SC_SVM || !mu || !gam || !dist) return SC_EARG;
+    const int d = h->prob.d, dd = h->dd;
+    const int64_t n = h->prob.n, n1 = h->prob.n1;
+    const double* W = h->pd_best.data();
+    const IterState st = *reinterpret_cast<const IterState*>(W + dd + (dd & 1));
+    const double er = st.eta / h->prob.rho;
+    double sP = 0, sQ = 0;
+    std::vector<double> e(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const bool P = i < n1;
+        double dW = 0;
+        for (int j = 0; j < d; ++j) dW = fma(h->X[i * d + j], W[j], dW);
+        double lg = -er * ((P ? 1.0 : -1.0) * dW - (P ? W[d] : W[d + 1]));
+        e[i] = exp(lg - st.shift);
+        (P ? sP : sQ) += e[i];
+    }
+    std::vector<double> z(d, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        if (i < n1) mu[i] = e[i] / sP; else gam[i - n1] = e[i] / sQ;
+    }
+    for (int64_t i = 0; i < n; ++i)
+        for (int j = 0; j < d; ++j)
+            z[j] += (i < n1 ? mu[i] : -gam[i - n1]) * h->X[i * d + j];
+    double s = 0;
+    for (int j = 0; j < d; ++j) s += z[j] * z[j];
+    *dist = sqrt(s);
+    return SC_OK;
+}
+
+int sc_iterate(sc_handle* h, double* p) {
+    (void)h; (void)p;
+    return SC_EARG;
+}
+
+int sc_set_grid(sc_handle* h, int32_t grid) { (void)h; (void)grid; return SC_OK; }
+
+int sc_info(const sc_handle* h, int64_t* out) {
+    if (!h || !out) return SC_EARG;
+    for (int i = 0; i < 8; ++i) out[i] = 0;
+    out[0] = 1; out[1] = 1;
+    return SC_OK;
+}
+
+const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+void sc_destroy(sc_handle* h) { delete h; }
+
+}  // extern "C"
