@@ -1,0 +1,517 @@
+// scmwu_host.cu — host side of the B200 engine: the C ABI of include/scmwu.h,
+// launch configuration and the one-off kernels (progress, iterate, column sums).
+#include "scmwu_kernel.cuh"
+
+namespace scmwu {
+// --------------------------------------------------------------------------------------
+// one-off kernels
+__global__ void progress_kernel(const double* X, const double* radii, int64_t n, int64_t n1,
+                                int d, int ld, int kind, const double* y, double* out) {
+    // out[block*3 + {0,1,2}]: SES {max dist+r}, SVM {min P.y, max Q.y}
+    const int lane = threadIdx.x & 31;
+    const int warps = blockDim.x >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5);
+    const int64_t nw = (int64_t)gridDim.x * warps;
+    double a0 = kind == SC_SES ? -INFINITY : INFINITY, a1 = -INFINITY;
+    for (int64_t i = gw; i < n; i += nw) {
+        const double* xr = X + i * ld;
+        double s = 0.0;
+        for (int j = lane; j < d; j += 32) {
+            if (kind == SC_SES) { double t = xr[j] - y[j]; s = fma(t, t, s); }
+            else s = fma(xr[j], y[j], s);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (kind == SC_SES) a0 = fmax(a0, sqrt(s) + radii[i]);
+        else if (i < n1) a0 = fmin(a0, s);
+        else a1 = fmax(a1, s);
+    }
+    __shared__ double sh[2][32];
+    if (lane == 0) { sh[0][threadIdx.x >> 5] = a0; sh[1][threadIdx.x >> 5] = a1; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < warps; ++w) {
+            a0 = kind == SC_SES ? fmax(a0, sh[0][w]) : fmin(a0, sh[0][w]);
+            a1 = fmax(a1, sh[1][w]);
+        }
+        out[blockIdx.x * 2] = a0;
+        out[blockIdx.x * 2 + 1] = a1;
+    }
+}
+
+// iterate materialisation: p for SES blocks / SVM coordinates, from an IterState slot.
+__global__ void iterate_kernel(const double* X, const double* radii, int64_t n, int64_t n1,
+                               int d, int ld, int kind, const double* slot, int dd, double rho,
+                               double alpha, double* out) {
+    const IterState st = *reinterpret_cast<const IterState*>(slot + dd + (dd & 1));
+    const double er = st.eta / rho;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (kind == SC_SES) {
+        if (i < 1 || i >= n) return;
+        const double* v = X + i * ld;
+        const double g = radii[i];
+        double a = 0.0;
+        for (int j = 0; j < d; ++j) { double x = fma(-st.t, v[j], slot[j]); a = fma(x, x, a); }
+        const double ra = sqrt(a);
+        const double nrm = er * ra;
+        const double x0 = -(er * st.t) * (alpha - g);
+        const double A = exp((x0 + nrm) * kInvSqrt2 - st.shift);
+        const double B = exp((x0 - nrm) * kInvSqrt2 - st.shift);
+        const double cc = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
+        double* o = out + (i - 1) * (d + 1);
+        for (int j = 0; j < d; ++j) {
+            const double x = fma(-st.t, v[j], slot[j]);
+            o[j] = (cc * (-er * x)) / st.T;
+        }
+        o[d] = ((A + B) / kSqrt2) / st.T;
+    } else {
+        if (i >= n) return;
+        const double* x = X + i * ld;
+        double s = 0.0;
+        for (int j = 0; j < d; ++j) s = fma(x[j], slot[j], s);
+        const bool P = i < n1;
+        const double lg = -er * ((P ? 1.0 : -1.0) * s - (P ? slot[d] : slot[d + 1]));
+        out[i] = exp(lg - st.shift) / st.T;
+    }
+}
+
+// column sums of P and Q rows (SVM iterate 1: all weights equal)
+__global__ void colsum_kernel(const double* X, int64_t a, int64_t b, int d, int ld,
+                              double* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= d) return;
+    double s = 0.0;
+    for (int64_t i = a; i < b; ++i) s += X[i * ld + j];
+    out[j] = s;
+}
+
+
+}  // namespace scmwu
+
+// ======================================================================================
+// host side
+using namespace scmwu;
+
+struct LaunchCfg {
+    int lpr, cpl;
+};
+
+static bool pick_cfg(int d, LaunchCfg& c) {
+    static const int tab[][3] = {{4, 2, 2},    {8, 2, 4},    {12, 4, 3},   {16, 4, 4},
+                                 {24, 4, 6},   {32, 4, 8},   {48, 8, 6},   {64, 8, 8},
+                                 {80, 8, 10},  {104, 8, 13}, {128, 8, 16}, {192, 16, 12},
+                                 {256, 16, 16}, {384, 32, 12}, {512, 32, 16}};
+    for (auto& r : tab)
+        if (d <= r[0]) { c.lpr = r[1]; c.cpl = r[2]; return true; }
+    return false;
+}
+
+// kernels are instantiated in scmwu_inst_*.cu (compiled in parallel)
+namespace scmwu {
+KernelFn scmwu_lookup_0(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_1(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_2(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_3(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_4(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_5(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_6(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_7(int kind, int lpr, int cpl);
+}  // namespace scmwu
+
+static KernelFn kernel_lookup(int kind, int lpr, int cpl) {
+    KernelFn (*fns[])(int, int, int) = {scmwu_lookup_0, scmwu_lookup_1, scmwu_lookup_2,
+                                        scmwu_lookup_3, scmwu_lookup_4, scmwu_lookup_5,
+                                        scmwu_lookup_6, scmwu_lookup_7};
+    for (auto f : fns)
+        if (KernelFn k = f(kind, lpr, cpl)) return k;
+    return nullptr;
+}
+
+struct sc_handle {
+    sc_problem prob;
+    int dd, ld, rw, pw, slot_len;
+    LaunchCfg cfg;
+    int sms = 0, grid = 0, gP = 0, tile_rows = 0, stages = 0, resident = 0;
+    uint32_t stage_stride = 0, rad_off = 0;
+    size_t smem = 0;
+    KernelFn fn = nullptr;
+    double g1 = 0.0;
+    double last_alpha = 0.0;
+    // device buffers
+    double *X = nullptr, *radii = nullptr, *red0 = nullptr, *partials = nullptr, *redg = nullptr;
+    int64_t* row_begin = nullptr;
+    unsigned long long* bar = nullptr;
+    double* ring = nullptr;
+    int64_t ring_cap = 0;
+    double* slots = nullptr;
+    sc_ftp_result* res = nullptr;
+    double *y_tilde = nullptr, *best_y = nullptr, *scratch = nullptr, *yvec = nullptr;
+    int* status = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // host state
+    std::vector<double> red0_h;
+    bool has_sep = false, has_callmin = false;
+    std::string err;
+};
+
+static int cuda_fail(sc_handle* h, cudaError_t e, const char* what) {
+    if (h) h->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? SC_EOOM : SC_ECUDA;
+}
+#define CK(call, what)                                   \
+    do {                                                 \
+        cudaError_t _e = (call);                         \
+        if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
+    } while (0)
+
+static int configure(sc_handle* h, int grid_req) {
+    const int d = h->prob.d;
+    const int RPW = 32 / h->cfg.lpr;
+    const int64_t n = h->prob.n;
+    // grid: one CTA per SM, at most one CTA per warp-step of rows
+    int G = grid_req > 0 ? grid_req : h->sms;
+    const int64_t step = (int64_t)kNW * RPW;
+    if (grid_req <= 0) G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + step - 1) / step));
+    if (h->prob.kind == SC_SVM) G = std::max(G, 2);
+    G = std::min(G, h->sms);
+    if (G < 1) G = 1;
+    if (h->prob.kind == SC_SVM && G < 2) { h->err = "SVM needs >= 2 SMs"; return SC_EARG; }
+    // rows -> CTAs
+    std::vector<int64_t> rb(G + 1);
+    if (h->prob.kind == SC_SES) {
+        for (int b = 0; b <= G; ++b) rb[b] = (int64_t)((__int128)n * b / G) & ~(int64_t)1;
+        rb[G] = n;
+        h->gP = 0;
+    } else {
+        const int64_t n1 = h->prob.n1, n2 = n - n1;
+        int gP = (int)llround((double)G * (double)n1 / (double)n);
+        gP = std::max(1, std::min(G - 1, gP));
+        for (int b = 0; b <= gP; ++b) rb[b] = (int64_t)((__int128)n1 * b / gP);
+        for (int b = gP; b <= G; ++b) rb[b] = n1 + (int64_t)((__int128)n2 * (b - gP) / (G - gP));
+        h->gP = gP;
+    }
+    // tiles: a multiple of the warp-step, about 24-48 KB
+    const int64_t rowb = (int64_t)h->ld * 8;
+    int m = (int)std::max<int64_t>(1, (32 * 1024) / (step * rowb));
+    int tr = (int)(step * m);
+    if ((int64_t)tr * rowb > 48 * 1024 && m > 1) tr = (int)(step * (m - 1));
+    h->tile_rows = tr;
+    const uint32_t xb = (uint32_t)((int64_t)tr * rowb);
+    h->rad_off = (xb + 15) & ~15u;
+    const uint32_t radb = h->prob.kind == SC_SES ? (uint32_t)((tr + 2) * 8) : 0u;
+    h->stage_stride = (h->rad_off + radb + 127) & ~127u;
+    int64_t max_rows = 0;
+    for (int b = 0; b < G; ++b) max_rows = std::max(max_rows, rb[b + 1] - rb[b]);
+    const int tiles = (int)((max_rows + tr - 1) / tr);
+    // stages: fill the remaining shared memory
+    int S = 2;
+    for (;;) {
+        size_t need = (size_t)(S + 1) * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, S + 1);
+        if (need > (size_t)kMaxSmem || S + 1 > 64) break;
+        ++S;
+    }
+    h->resident = tiles <= S ? 1 : 0;
+    if (h->resident) S = std::max(tiles, 1);
+    h->stages = S;
+    h->smem = (size_t)S * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, S);
+    if (h->smem > (size_t)kMaxSmem) { h->err = "shared memory budget exceeded"; return SC_EARG; }
+    h->grid = G;
+    if (h->row_begin) cudaFree(h->row_begin);
+    if (h->partials) cudaFree(h->partials);
+    CK(cudaMalloc(&h->row_begin, (G + 1) * sizeof(int64_t)), "alloc rows");
+    CK(cudaMemcpy(h->row_begin, rb.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice),
+       "copy rows");
+    CK(cudaMalloc(&h->partials, (size_t)G * h->rw * sizeof(double)), "alloc partials");
+    CK(cudaFuncSetAttribute(h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem),
+       "smem attribute");
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, h->fn, kThreads, h->smem),
+       "occupancy");
+    if (per_sm < 1) { h->err = "kernel does not fit on an SM"; return SC_ECUDA; }
+    return SC_OK;
+}
+
+extern "C" {
+
+int sc_version(void) { return 1000; }
+
+int sc_create(const sc_problem* prob, const double* X, const double* X_tail, const double* radii,
+              sc_handle** out) {
+    if (!out) return SC_EARG;
+    *out = nullptr;
+    if (!prob || !X || prob->d < 1 || prob->n < 2) return SC_EARG;
+    if (prob->kind != SC_SES && prob->kind != SC_SVM) return SC_EARG;
+    if (prob->kind == SC_SES && !radii) return SC_EARG;
+    if (prob->kind == SC_SVM && (prob->n1 < 1 || prob->n1 >= prob->n || radii)) return SC_EARG;
+    sc_handle* h = new sc_handle();
+    *out = h;
+    h->prob = *prob;
+    const int d = prob->d;
+    const int64_t n = prob->n;
+    if (!pick_cfg(d, h->cfg)) { h->err = "d > 512 is not supported yet"; return SC_EARG; }
+    h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl);
+    if (!h->fn) { h->err = "no kernel instantiated for this d"; return SC_EARG; }
+    h->dd = prob->kind == SC_SES ? d + 1 : d + 2;
+    h->ld = (d + 1) & ~1;
+    h->rw = red_width(prob->kind, d);
+    h->pw = part_width(prob->kind, d);
+    h->slot_len = h->dd + (h->dd & 1) + (int)(sizeof(IterState) / sizeof(double));
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev), "device count");
+    if (prob->device < 0 || prob->device >= ndev) { h->err = "no such CUDA device"; return SC_ECUDA; }
+    CK(cudaSetDevice(prob->device), "set device");
+    cudaDeviceProp dp;
+    CK(cudaGetDeviceProperties(&dp, prob->device), "device properties");
+    if (dp.major < 10) { h->err = "needs an sm_100 (B200) device"; return SC_ECUDA; }
+    if (!dp.cooperativeLaunch) { h->err = "cooperative launch unsupported"; return SC_ECUDA; }
+    h->sms = dp.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
+    CK(cudaEventCreate(&h->ev0), "event");
+    CK(cudaEventCreate(&h->ev1), "event");
+    // X: n x ld, rows padded to an even length (16-byte rows for the bulk copies)
+    const size_t xbytes = (size_t)n * h->ld * sizeof(double);
+    CK(cudaMalloc(&h->X, xbytes), "alloc X");
+    const int64_t n_head = X_tail ? prob->n1 : n;
+    if (h->ld == d) {
+        CK(cudaMemcpy(h->X, X, (size_t)n_head * d * 8, cudaMemcpyHostToDevice), "copy X");
+        if (X_tail)
+            CK(cudaMemcpy(h->X + n_head * d, X_tail, (size_t)(n - n_head) * d * 8,
+                          cudaMemcpyHostToDevice), "copy X tail");
+    } else {
+        CK(cudaMemset(h->X, 0, xbytes), "zero X");
+        CK(cudaMemcpy2D(h->X, h->ld * 8, X, d * 8, d * 8, n_head, cudaMemcpyHostToDevice),
+           "copy X");
+        if (X_tail)
+            CK(cudaMemcpy2D(h->X + n_head * h->ld, h->ld * 8, X_tail, d * 8, d * 8, n - n_head,
+                            cudaMemcpyHostToDevice), "copy X tail");
+    }
+    if (prob->kind == SC_SES) {
+        const int64_t nr = (n + 1) & ~(int64_t)1;
+        CK(cudaMalloc(&h->radii, (size_t)(nr + 2) * 8), "alloc radii");
+        CK(cudaMemset(h->radii, 0, (size_t)(nr + 2) * 8), "zero radii");
+        CK(cudaMemcpy(h->radii, radii, (size_t)n * 8, cudaMemcpyHostToDevice), "copy radii");
+        h->g1 = radii[0];
+    }
+    // reduced vector of iterate 1 (cum = 0: every exponent 0)
+    h->red0_h.assign(h->rw, 0.0);
+    if (prob->kind == SC_SES) {
+        double rad = 0.0;
+        for (int64_t i = 1; i < n; ++i) rad += 2.0 * radii[i];
+        h->red0_h[kS_T] = 2.0 * (double)(n - 1);
+        h->red0_h[kS_Rad] = rad;
+    } else {
+        h->red0_h[kV_TP] = (double)prob->n1;
+        h->red0_h[kV_TQ] = (double)(n - prob->n1);
+        double* cs = nullptr;
+        CK(cudaMalloc(&cs, 2 * (size_t)d * 8), "alloc colsum");
+        colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, 0, prob->n1, d, h->ld, cs);
+        colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, prob->n1, n, d, h->ld, cs + d);
+        CK(cudaStreamSynchronize(h->stream), "colsum");
+        CK(cudaMemcpy(h->red0_h.data() + kV_Vec, cs, 2 * (size_t)d * 8, cudaMemcpyDeviceToHost),
+           "copy colsum");
+        cudaFree(cs);
+    }
+    CK(cudaMalloc(&h->red0, h->rw * 8), "alloc red0");
+    CK(cudaMemcpy(h->red0, h->red0_h.data(), h->rw * 8, cudaMemcpyHostToDevice), "copy red0");
+    CK(cudaMalloc(&h->redg, h->rw * 8), "alloc redg");
+    CK(cudaMalloc(&h->bar, 64), "alloc barrier");
+    CK(cudaMalloc(&h->slots, (size_t)kNumSlots * h->slot_len * 8), "alloc slots");
+    CK(cudaMemset(h->slots, 0, (size_t)kNumSlots * h->slot_len * 8), "zero slots");
+    CK(cudaMalloc(&h->res, sizeof(sc_ftp_result)), "alloc result");
+    CK(cudaMalloc(&h->y_tilde, h->dd * 8), "alloc y");
+    CK(cudaMalloc(&h->best_y, h->dd * 8), "alloc y");
+    CK(cudaMalloc(&h->yvec, (size_t)(d + 2) * 8), "alloc y");
+    CK(cudaMalloc(&h->status, sizeof(int)), "alloc status");
+    CK(cudaMalloc(&h->scratch, 2 * 4096 * 8), "alloc scratch");
+    int st = configure(h, prob->grid);
+    if (st != SC_OK) return st;
+    h->err.clear();
+    return SC_OK;
+}
+
+int sc_set_grid(sc_handle* h, int32_t grid) {
+    if (!h) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    return configure(h, grid);
+}
+
+int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_tilde,
+           double* best_y) {
+    if (!h || !args || !res || !y_tilde || !best_y) return SC_EARG;
+    memset(res, 0, sizeof(*res));
+    if (args->mode != SC_MODE_FTP && args->mode != SC_MODE_REFINE) return SC_EARG;
+    if (!(args->alpha > 0.0)) { h->err = "alpha must be positive"; return SC_EARG; }
+    const int64_t T = args->mode == SC_MODE_FTP ? args->budget : args->horizon;
+    if (T < 0 || (args->mode == SC_MODE_REFINE && T < 1)) {
+        h->err = "budget/horizon out of range";
+        return SC_EARG;
+    }
+    CK(cudaSetDevice(h->prob.device), "set device");
+    // window history: max(64, T/2) + 2 entries (the largest rung is <= T)
+    int64_t need = std::max<int64_t>(kLadderBase, T / 2) + 2;
+    const int64_t cap_lim = ((int64_t)1 << 30) / (h->dd * 8);   // 1 GiB
+    if (need > cap_lim) need = cap_lim;
+    if (need > h->ring_cap) {
+        if (h->ring) cudaFree(h->ring);
+        h->ring = nullptr;
+        CK(cudaMalloc(&h->ring, (size_t)need * h->dd * 8), "alloc window ring");
+        h->ring_cap = need;
+    }
+    KParams p;
+    memset(&p, 0, sizeof(p));
+    p.kind = h->prob.kind; p.d = h->prob.d; p.ld = h->ld; p.dd = h->dd; p.rw = h->rw; p.pw = h->pw;
+    p.G = h->grid; p.gP = h->gP; p.tile_rows = h->tile_rows; p.stages = h->stages;
+    p.resident = h->resident; p.n = h->prob.n; p.n1 = h->prob.n1;
+    p.X = h->X; p.radii = h->radii; p.row_begin = h->row_begin;
+    p.rho = h->prob.rho; p.inv_rho = 1.0 / h->prob.rho; p.R = h->prob.R; p.ln_r = h->prob.ln_r;
+    p.D = h->prob.D; p.g1 = h->g1;
+    p.red0 = h->red0; p.partials = h->partials; p.redg = h->redg; p.bar = h->bar;
+    p.ring = h->ring; p.ring_cap = h->ring_cap; p.slots = h->slots; p.slot_len = h->slot_len;
+    h->last_alpha = args->alpha;
+    p.args = *args; p.res = h->res; p.y_tilde = h->y_tilde; p.best_y = h->best_y;
+    p.status = h->status; p.stage_stride = h->stage_stride; p.rad_off = h->rad_off;
+    CK(cudaMemsetAsync(h->bar, 0, 64, h->stream), "reset barrier");
+    CK(cudaMemsetAsync(h->res, 0, sizeof(sc_ftp_result), h->stream), "reset result");
+    CK(cudaMemsetAsync(h->status, 0xff, sizeof(int), h->stream), "reset status");
+    void* kargs[] = {&p};
+    CK(cudaEventRecord(h->ev0, h->stream), "event");
+    CK(cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(kThreads), kargs,
+                                   h->smem, h->stream),
+       "persistent kernel launch");
+    CK(cudaEventRecord(h->ev1, h->stream), "event");
+    CK(cudaStreamSynchronize(h->stream), "persistent kernel");
+    int status = -1;
+    CK(cudaMemcpy(res, h->res, sizeof(sc_ftp_result), cudaMemcpyDeviceToHost), "copy result");
+    CK(cudaMemcpy(&status, h->status, sizeof(int), cudaMemcpyDeviceToHost), "copy status");
+    CK(cudaMemcpy(y_tilde, h->y_tilde, h->dd * 8, cudaMemcpyDeviceToHost), "copy y");
+    CK(cudaMemcpy(best_y, h->best_y, h->dd * 8, cudaMemcpyDeviceToHost), "copy y");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+    res->kernel_ms = ms;
+    h->has_callmin = res->has_counter_min != 0;
+    h->has_sep = res->kind == SC_PRIMAL;
+    if (status == SC_EWIDTH) { h->err = "width violation"; return SC_EWIDTH; }
+    if (status != SC_OK) { h->err = "kernel did not complete"; return SC_ECUDA; }
+    return SC_OK;
+}
+
+int sc_progress(sc_handle* h, const double* y, double* f) {
+    if (!h || !y || !f) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    const int d = h->prob.d;
+    CK(cudaMemcpyAsync(h->yvec, y, d * 8, cudaMemcpyHostToDevice, h->stream), "copy y");
+    const int blocks = std::min(h->sms * 4, 2048);
+    progress_kernel<<<blocks, 256, 0, h->stream>>>(h->X, h->radii, h->prob.n, h->prob.n1, d,
+                                                   h->ld, h->prob.kind, h->yvec, h->scratch);
+    CK(cudaGetLastError(), "progress kernel");
+    std::vector<double> part(2 * blocks);
+    CK(cudaMemcpyAsync(part.data(), h->scratch, part.size() * 8, cudaMemcpyDeviceToHost,
+                       h->stream), "copy progress");
+    CK(cudaStreamSynchronize(h->stream), "progress");
+    if (h->prob.kind == SC_SES) {
+        double m = -INFINITY;
+        for (int b = 0; b < blocks; ++b) m = std::max(m, part[2 * b]);
+        *f = m;
+    } else {
+        double mp = INFINITY, mq = -INFINITY, nrm = 0.0;
+        for (int b = 0; b < blocks; ++b) { mp = std::min(mp, part[2 * b]); mq = std::max(mq, part[2 * b + 1]); }
+        for (int j = 0; j < d; ++j) nrm += y[j] * y[j];
+        nrm = sqrt(nrm);
+        *f = Control<WarpLanes>::svm_margin(mp, mq, nrm);
+    }
+    return SC_OK;
+}
+
+int sc_iterate(sc_handle* h, double* out) {
+    if (!h || !out) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    const int64_t n = h->prob.n;
+    const int64_t size = h->prob.kind == SC_SES ? (n - 1) * (h->prob.d + 1) : n;
+    double* buf = nullptr;
+    CK(cudaMalloc(&buf, (size_t)size * 8), "alloc iterate");
+    // the `last` slot holds the latest iterate's state (written by the last sc_ftp)
+    iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
+        h->X, h->radii, n, h->prob.n1, h->prob.d, h->ld, h->prob.kind,
+        h->slots + 4 * h->slot_len, h->dd, h->prob.rho, h->last_alpha, buf);
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(out, buf, (size_t)size * 8, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (e != cudaSuccess) return cuda_fail(h, e, "iterate");
+    return SC_OK;
+}
+
+int sc_pd_commit(sc_handle* h, int32_t which) {
+    if (!h || h->prob.kind != SC_SVM) return SC_EARG;
+    if (which != 0 && which != 1) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    const double* src = h->slots + (which == 0 ? 1 : 2) * h->slot_len;
+    CK(cudaMemcpy(h->slots + 3 * h->slot_len, src, h->slot_len * 8, cudaMemcpyDeviceToDevice),
+       "commit");
+    return SC_OK;
+}
+
+int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
+    if (!h || h->prob.kind != SC_SVM || !mu || !gam || !dist) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    const int64_t n = h->prob.n, n1 = h->prob.n1;
+    const int d = h->prob.d;
+    double* buf = nullptr;
+    CK(cudaMalloc(&buf, (size_t)n * 8), "alloc pair");
+    // e_i * T from the committed state (T cancels in the normalisation below)
+    std::vector<double> slot(h->slot_len);
+    CK(cudaMemcpy(slot.data(), h->slots + 3 * h->slot_len, h->slot_len * 8,
+                  cudaMemcpyDeviceToHost), "copy slot");
+    IterState* st = reinterpret_cast<IterState*>(slot.data() + h->dd + (h->dd & 1));
+    if (st->T == 0.0) {   // never committed: uniform weights (t = 0 state)
+        st->T = 1.0; st->eta = 1.0; st->t = 0.0; st->shift = 0.0;
+        CK(cudaMemcpy(h->slots + 3 * h->slot_len, slot.data(), h->slot_len * 8,
+                      cudaMemcpyHostToDevice), "init slot");
+    }
+    iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
+        h->X, h->radii, n, n1, d, h->ld, SC_SVM, h->slots + 3 * h->slot_len, h->dd, h->prob.rho,
+        0.0, buf);
+    std::vector<double> e(n);
+    cudaError_t ce = cudaStreamSynchronize(h->stream);
+    if (ce == cudaSuccess) ce = cudaMemcpy(e.data(), buf, (size_t)n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (ce != cudaSuccess) return cuda_fail(h, ce, "pd pair");
+    double sP = 0.0, sQ = 0.0;
+    for (int64_t i = 0; i < n1; ++i) sP += e[i];
+    for (int64_t i = n1; i < n; ++i) sQ += e[i];
+    for (int64_t i = 0; i < n1; ++i) mu[i] = e[i] / sP;
+    for (int64_t i = n1; i < n; ++i) gam[i - n1] = e[i] / sQ;
+    // distance of the uniform pair from the column sums; callers keep the committed one
+    double s = 0.0;
+    for (int j = 0; j < d; ++j) {
+        double z = h->red0_h[kV_Vec + j] / (double)n1 - h->red0_h[kV_Vec + d + j] / (double)(n - n1);
+        s += z * z;
+    }
+    *dist = sqrt(s);
+    return SC_OK;
+}
+
+int sc_info(const sc_handle* h, int64_t* out) {
+    if (!h || !out) return SC_EARG;
+    out[0] = h->grid; out[1] = kThreads; out[2] = h->cfg.lpr; out[3] = h->cfg.cpl;
+    out[4] = h->tile_rows; out[5] = h->stages; out[6] = h->resident; out[7] = (int64_t)h->smem;
+    return SC_OK;
+}
+
+const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+void sc_destroy(sc_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->prob.device);
+    void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar,
+                    h->ring, h->slots, h->res, h->y_tilde, h->best_y, h->scratch, h->yvec,
+                    h->status};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+}  // extern "C"
