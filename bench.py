@@ -1,0 +1,328 @@
+"""Benchmark: time-to-eps of the SCMWU solvers on the B200 engine.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ses_c2|svm_c3|ses_c1|ses_c4]
+    python bench.py --impl reference ...      # CPU reference arm (the oracle port)
+
+A *step* is one full solve (adaptive search to the reference's stopping rule)
+of the workload BASELINE.json's metric is quoted on: by default configs[1],
+SES n=10^6, d=100 uniform-ball points, eps=1e-3 on one B200.
+
+value    time-to-eps with the instance already resident in HBM, device-timed
+         with CUDA events on the engine's stream (host gaps between kernel
+         launches included), max over ranks.
+e2e      the same solve through the public API (solve_ses / solve_svm) from
+         host numpy arrays: H2D of the instance and D2H of the result inside.
+roofline HBM roofline of the persistent kernel: algorithmic bytes
+         8 n (d+1) (SES) or 8 n d (SVM) per streaming pass x passes / kernel
+         event time, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the oracle port (oracle/, numpy + C restatement of the reference)
+         timed on this host for a bounded sample of iterations of the same
+         workload; time-to-eps extrapolated as s/iter x GPU iterations.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "ses_c2": dict(kind="ses", n=10 ** 6, d=100, dist="uniform-ball", seed=0, eps=1e-3,
+                   desc="SES n=10^6 d=100 uniform-in-ball points, eps=1e-3 (BASELINE configs[1])"),
+    "svm_c3": dict(kind="svm", n1=500_000, n2=500_000, d=100, seed=0, gap=1.0, eps=1e-3,
+                   desc="hard-margin SVM n=10^6 (5e5+5e5) d=100 gap 1, eps=1e-3 (configs[2])"),
+    "ses_c1": dict(kind="ses", n=10_000, d=10, dist="gaussian", seed=0, eps=1e-2,
+                   desc="SES n=10^4 d=10 Gaussian, eps=1e-2 (configs[0])"),
+    "ses_c4": dict(kind="ses", n=10 ** 7, d=100, dist="uniform-ball", seed=0, eps=1e-3,
+                   desc="SES n=10^7 d=100 uniform-in-ball, eps=1e-3 (configs[3])"),
+}
+# GPU iteration counts of full solves measured by this bench (profiles/); used only by the
+# reference arm to extrapolate the CPU port's s/iter to a time-to-eps.
+ITERS_EST = {"ses_c2": 360_000, "svm_c3": 300_000, "ses_c1": 82_518, "ses_c4": 360_000}
+
+
+def make_instance(w):
+    from paper_2405_09157_b200 import instances
+    if w["kind"] == "ses":
+        return instances.gen_ses(w["n"], w["d"], w["seed"], w["dist"])
+    inst, _ = instances.gen_svm(w["n1"], w["n2"], w["d"], w["seed"], w["gap"])
+    return inst
+
+
+def alg_bytes_per_pass(w):
+    if w["kind"] == "ses":
+        return 8 * w["n"] * (w["d"] + 1)
+    return 8 * (w["n1"] + w["n2"]) * w["d"]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ CPU (oracle port) sample
+def cpu_sample(w, inst, max_seconds=20.0, max_iters=64):
+    """Time the oracle port for a bounded number of MWU iterations of the workload:
+    a bracketing-phase feasibility test at the first level the search would try."""
+    import oracle as O
+    t_setup = time.perf_counter()
+    if w["kind"] == "ses":
+        prob = O.SesProblem(inst.centers, inst.radii)
+        D, L0, U0 = prob.range()
+        spec = prob.spec(3.0 * D / math.sqrt(2.0))
+        alpha = L0 + (U0 - L0) / 3.0
+        progress = (lambda y: prob.progress(y[:w["d"]]))
+    else:
+        prob = O.SvmProblem(inst.P, inst.Q)
+        spec = prob.spec()
+        alpha = 2.0 * 2.0 * prob.D / 3.0
+        progress = (lambda y: prob.progress(y[:w["d"]]))
+    setup = time.perf_counter() - t_setup
+    # calibrate: 2 iterations, then as many as fit in max_seconds
+    t0 = time.perf_counter()
+    O.ftp(spec, alpha, 0.25, progress=progress, cap=2)
+    per = (time.perf_counter() - t0) / 2.0
+    k = int(max(2, min(max_iters, max_seconds / max(per, 1e-9))))
+    t0 = time.perf_counter()
+    res = O.ftp(spec, alpha, 0.25, progress=progress, cap=k)
+    dt = time.perf_counter() - t0
+    return {"s_per_iter": dt / res.iterations, "iters": res.iterations, "seconds": dt,
+            "setup_s": setup}
+
+
+def reference_arm(args, w, rank):
+    if rank != 0:
+        return
+    inst = make_instance(w)
+    t0 = time.perf_counter()
+    samples = []
+    for _ in range(args.warmup):
+        cpu_sample(w, inst, max_seconds=3.0, max_iters=4)
+    for _ in range(args.steps):
+        samples.append(cpu_sample(w, inst, max_seconds=20.0))
+    spi = statistics.median(s["s_per_iter"] for s in samples)
+    iters = ITERS_EST[args.workload]
+    value = spi * iters
+    line = {
+        "impl": "reference", "metric": "time-to-eps (s)", "value": value, "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value * 1000.0, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w["desc"], "eps": w["eps"], "seed": w["seed"],
+                   "extrapolated_from_iters": iters},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "port",
+                         "sample": f"{samples[-1]['iters']} MWU iterations of one feasibility "
+                                   f"test of the workload per step; {spi:.4f} s/iter x "
+                                   f"{iters} iterations (extrapolated)"},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def solve(w, inst, device=None):
+    from paper_2405_09157_b200 import ses, svm
+    if w["kind"] == "ses":
+        return ses.solve_ses(inst, w["eps"], device=device)
+    return svm.solve_svm(inst, w["eps"], device=device)
+
+
+def our_arm(args, w, rank, world):
+    import torch
+    from paper_2405_09157_b200 import ses, svm
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    inst = make_instance(w)
+    t_up = time.perf_counter()
+    dev = (ses.ses_device(inst, device=local) if w["kind"] == "ses"
+           else svm.svm_device(inst, device=local))
+    upload_s = time.perf_counter() - t_up
+    info = dev.handle.info()
+    for _ in range(args.warmup):
+        solve(w, inst, dev)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            tdist.barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    l0 = dev.handle.launches()
+    reports = []
+    times = []
+    for _ in range(args.steps):
+        dev.handle.mark(0)
+        rep, sol = solve(w, inst, dev)
+        dev.handle.mark(1)
+        times.append(dev.handle.elapsed_ms() / 1000.0)
+        reports.append((rep, sol))
+    barrier()
+    launches = dev.handle.launches() - l0
+    clk = clocks.stop()
+    t_step = max(times)
+    if dist:
+        t = torch.tensor([t_step], device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        t_step = float(t.item())
+    kernel_s = sum(r.kernel_ms for r, _ in reports) / 1000.0
+    passes = sum(r.passes for r, _ in reports)
+    dev.close()
+
+    # e2e: public API from host arrays (upload + download inside the timed region)
+    e2e_times = []
+    for _ in range(max(1, args.steps)):
+        barrier()
+        t0 = time.perf_counter()
+        rep_e, sol_e = solve(w, inst, None)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    e2e = max(e2e_times)
+    if w["kind"] == "ses":
+        h2d = inst.centers.nbytes + inst.radii.nbytes
+        d2h = (w["d"] + 1) * 8 * 2 * rep_e.search_steps + 8 * 4
+    else:
+        h2d = inst.P.nbytes + inst.Q.nbytes
+        d2h = (w["d"] + 2) * 8 * 2 * rep_e.search_steps + inst.n1 * 8 + inst.n2 * 8
+
+    peak, peak_kind = measured_peak()
+    achieved = passes * alg_bytes_per_pass(w) / kernel_s / 1e9 if kernel_s > 0 else 0.0
+    rep0, sol0 = reports[-1]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_pass")
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": "time-to-eps (s)", "value": t_step, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1000.0,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": w["desc"], "eps": w["eps"], "seed": w["seed"],
+                   "iterations": rep0.total_iterations, "search_steps": rep0.search_steps,
+                   "termination": rep0.termination.value,
+                   "l2": "inputs larger than L2 (X = %.0f MB)" % (alg_bytes_per_pass(w) / 1e6)
+                   if alg_bytes_per_pass(w) > 126e6 else "inputs fit in L2",
+                   "kernel": info, "upload_s": upload_s},
+        "result": ({"radius": sol0.radius, "lower": rep0.primal_value,
+                    "enclosure_slack": sol0.enclosure_slack} if w["kind"] == "ses" else
+                   {"margin": sol0.margin, "pd_distance": sol0.pd_distance}),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "alg_bytes_per_pass": alg_bytes_per_pass(w),
+                     "us_per_pass": kernel_s / passes * 1e6 if passes else None,
+                     "kernel_s": kernel_s, "passes": passes},
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        s = cpu_sample(w, inst, max_seconds=args.cpu_seconds)
+        its = rep0.total_iterations
+        line["cpu_baseline"] = {
+            "value": s["s_per_iter"] * its, "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"{s['iters']} MWU iterations of the workload's first bracketing test "
+                      f"on the oracle port ({s['s_per_iter']:.4f} s/iter); time-to-eps "
+                      f"extrapolated x {its} GPU iterations"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="ses_c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        reference_arm(args, w, rank)
+    else:
+        our_arm(args, w, rank, world)
+
+
+if __name__ == "__main__":
+    main()

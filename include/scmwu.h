@@ -121,7 +121,15 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
            double* y_tilde /* dual_dim */, double* best_y /* dual_dim */);
 int sc_progress(sc_handle* h, const double* y /* d values */, double* f);
 int sc_iterate(sc_handle* h, double* p /* SES (n-1)(d+1), SVM n */);
-int sc_pd_commit(sc_handle* h, int32_t which /* 0: call minimum, 1: separating iterate */);
+int sc_pd_commit(sc_handle* h, int32_t which /* 0: call minimum, 1: separating iterate,
+                                                2: reset to the uniform pair */);
+/* Device-side timing of a span of calls: sc_mark(h, 0) records a CUDA event on the
+ * handle's stream, sc_mark(h, 1) another one and waits for it; sc_elapsed returns
+ * the milliseconds between them (host gaps between launches included). */
+int sc_mark(sc_handle* h, int32_t which);
+int sc_elapsed(sc_handle* h, float* ms);
+/* Kernel launches issued by this handle since creation (persistent + one-off). */
+int64_t sc_launches(const sc_handle* h);
 int sc_pd_pair(sc_handle* h, double* mu /* n1 */, double* gam /* n - n1 */, double* dist);
 int sc_set_grid(sc_handle* h, int32_t grid);
 int sc_info(const sc_handle* h, int64_t* out /* 8 values: grid, threads, lanes_per_row,

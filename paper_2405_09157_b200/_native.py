@@ -65,7 +65,8 @@ class ScFtpResult(ctypes.Structure):
 
 
 EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "sc_pd_pair",
-           "sc_set_grid", "sc_info", "sc_last_error", "sc_destroy", "sc_version")
+           "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_last_error",
+           "sc_destroy", "sc_version")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -101,6 +102,10 @@ class Engine:
         lib.sc_destroy.argtypes = [vp]
         lib.sc_destroy.restype = None
         lib.sc_version.restype = ctypes.c_int
+        lib.sc_mark.argtypes = [vp, ctypes.c_int32]
+        lib.sc_elapsed.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+        lib.sc_launches.argtypes = [vp]
+        lib.sc_launches.restype = ctypes.c_int64
         self.lib = lib
 
     def create(self, kind: int, X, X_tail, radii, D: float, rho: float, R: float,
@@ -198,6 +203,20 @@ class Handle:
         self._check(self.engine.lib.sc_pd_pair(self.h, _ptr(mu), _ptr(gam), ctypes.byref(dist)),
                     "sc_pd_pair")
         return mu, gam, float(dist.value)
+
+    def pd_reset(self) -> None:
+        self._check(self.engine.lib.sc_pd_commit(self.h, 2), "sc_pd_commit")
+
+    def mark(self, which: int) -> None:
+        self._check(self.engine.lib.sc_mark(self.h, which), "sc_mark")
+
+    def elapsed_ms(self) -> float:
+        ms = ctypes.c_float()
+        self._check(self.engine.lib.sc_elapsed(self.h, ctypes.byref(ms)), "sc_elapsed")
+        return float(ms.value)
+
+    def launches(self) -> int:
+        return int(self.engine.lib.sc_launches(self.h))
 
     def set_grid(self, grid: int) -> None:
         self._check(self.engine.lib.sc_set_grid(self.h, grid), "sc_set_grid")

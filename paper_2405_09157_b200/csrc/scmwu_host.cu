@@ -148,7 +148,8 @@ struct sc_handle {
     double *y_tilde = nullptr, *best_y = nullptr, *scratch = nullptr, *yvec = nullptr;
     int* status = nullptr;
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, mk0 = nullptr, mk1 = nullptr;
+    int64_t launches = 0;
     // host state
     std::vector<double> red0_h;
     bool has_sep = false, has_callmin = false;
@@ -269,6 +270,8 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail, con
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
     CK(cudaEventCreate(&h->ev0), "event");
     CK(cudaEventCreate(&h->ev1), "event");
+    CK(cudaEventCreate(&h->mk0), "event");
+    CK(cudaEventCreate(&h->mk1), "event");
     // X: n x ld, rows padded to an even length (16-byte rows for the bulk copies)
     const size_t xbytes = (size_t)n * h->ld * sizeof(double);
     CK(cudaMalloc(&h->X, xbytes), "alloc X");
@@ -379,6 +382,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     CK(cudaLaunchCooperativeKernel((const void*)h->fn, dim3(h->grid), dim3(kThreads), kargs,
                                    h->smem, h->stream),
        "persistent kernel launch");
+    h->launches += 1;
     CK(cudaEventRecord(h->ev1, h->stream), "event");
     CK(cudaStreamSynchronize(h->stream), "persistent kernel");
     int status = -1;
@@ -404,6 +408,7 @@ int sc_progress(sc_handle* h, const double* y, double* f) {
     const int blocks = std::min(h->sms * 4, 2048);
     progress_kernel<<<blocks, 256, 0, h->stream>>>(h->X, h->radii, h->prob.n, h->prob.n1, d,
                                                    h->ld, h->prob.kind, h->yvec, h->scratch);
+    h->launches += 1;
     CK(cudaGetLastError(), "progress kernel");
     std::vector<double> part(2 * blocks);
     CK(cudaMemcpyAsync(part.data(), h->scratch, part.size() * 8, cudaMemcpyDeviceToHost,
@@ -434,6 +439,7 @@ int sc_iterate(sc_handle* h, double* out) {
     iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
         h->X, h->radii, n, h->prob.n1, h->prob.d, h->ld, h->prob.kind,
         h->slots + 4 * h->slot_len, h->dd, h->prob.rho, h->last_alpha, buf);
+    h->launches += 1;
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e == cudaSuccess) e = cudaMemcpy(out, buf, (size_t)size * 8, cudaMemcpyDeviceToHost);
     cudaFree(buf);
@@ -443,8 +449,12 @@ int sc_iterate(sc_handle* h, double* out) {
 
 int sc_pd_commit(sc_handle* h, int32_t which) {
     if (!h || h->prob.kind != SC_SVM) return SC_EARG;
-    if (which != 0 && which != 1) return SC_EARG;
+    if (which != 0 && which != 1 && which != 2) return SC_EARG;
     CK(cudaSetDevice(h->prob.device), "set device");
+    if (which == 2) {   // back to the t = 0 state (uniform pair)
+        CK(cudaMemset(h->slots + 3 * h->slot_len, 0, h->slot_len * 8), "reset pair");
+        return SC_OK;
+    }
     const double* src = h->slots + (which == 0 ? 1 : 2) * h->slot_len;
     CK(cudaMemcpy(h->slots + 3 * h->slot_len, src, h->slot_len * 8, cudaMemcpyDeviceToDevice),
        "commit");
@@ -471,6 +481,7 @@ int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
     iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
         h->X, h->radii, n, n1, d, h->ld, SC_SVM, h->slots + 3 * h->slot_len, h->dd, h->prob.rho,
         0.0, buf);
+    h->launches += 1;
     std::vector<double> e(n);
     cudaError_t ce = cudaStreamSynchronize(h->stream);
     if (ce == cudaSuccess) ce = cudaMemcpy(e.data(), buf, (size_t)n * 8, cudaMemcpyDeviceToHost);
@@ -498,6 +509,22 @@ int sc_info(const sc_handle* h, int64_t* out) {
     return SC_OK;
 }
 
+int sc_mark(sc_handle* h, int32_t which) {
+    if (!h || (which != 0 && which != 1)) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    CK(cudaEventRecord(which == 0 ? h->mk0 : h->mk1, h->stream), "mark");
+    if (which == 1) CK(cudaEventSynchronize(h->mk1), "mark");
+    return SC_OK;
+}
+
+int sc_elapsed(sc_handle* h, float* ms) {
+    if (!h || !ms) return SC_EARG;
+    CK(cudaEventElapsedTime(ms, h->mk0, h->mk1), "elapsed");
+    return SC_OK;
+}
+
+int64_t sc_launches(const sc_handle* h) { return h ? h->launches : 0; }
+
 const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 void sc_destroy(sc_handle* h) {
@@ -510,6 +537,8 @@ void sc_destroy(sc_handle* h) {
         if (b) cudaFree(b);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->mk0) cudaEventDestroy(h->mk0);
+    if (h->mk1) cudaEventDestroy(h->mk1);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }

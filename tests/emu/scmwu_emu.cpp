@@ -248,6 +248,7 @@ int sc_pd_commit(sc_handle* h, int32_t which) {
     if (!h || h->prob.kind != SC_SVM) return SC_EARG;
     if (which == 0) h->pd_best = h->pd_callmin;
     else if (which == 1) h->pd_best = h->pd_sep;
+    else if (which == 2) h->pd_best.assign(h->pd_best.size(), 0.0);
     else return SC_EARG;
     return SC_OK;
 }
@@ -295,6 +296,14 @@ int sc_info(const sc_handle* h, int64_t* out) {
     out[0] = 1; out[1] = 1;
     return SC_OK;
 }
+
+int sc_mark(sc_handle* h, int32_t which) { return h && (which == 0 || which == 1) ? SC_OK : SC_EARG; }
+int sc_elapsed(sc_handle* h, float* ms) {
+    if (!h || !ms) return SC_EARG;
+    *ms = 0.0f;
+    return SC_OK;
+}
+int64_t sc_launches(const sc_handle* h) { (void)h; return 0; }
 
 const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "null handle"; }
 

@@ -1,0 +1,63 @@
+"""Per-pass throughput of the persistent kernel on the BASELINE workloads (dev tool).
+
+    python tools/gpu_perf.py [ses_c2|svm_c3|ses_c1|...] [--full] [--grid G]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2405_09157_b200 import meta, ses, svm  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("workload", nargs="?", default="ses_c2")
+    ap.add_argument("--full", action="store_true")
+    ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--horizon", type=int, default=2048)
+    a = ap.parse_args()
+    w = bench.WORKLOADS[a.workload]
+    t0 = time.time()
+    inst = bench.make_instance(w)
+    print(f"gen {time.time()-t0:.1f}s", flush=True)
+    t0 = time.time()
+    if w["kind"] == "ses":
+        dev = ses.ses_device(inst, grid=a.grid)
+        D, L0, U0 = ses.ses_range(inst)
+        spec = meta.OracleSpec(dev.cone, 3 * D / math.sqrt(2), w["d"] + 1, dev, math.sqrt(2),
+                               meta.Orientation.MAX)
+        alpha = 0.5 * (L0 + U0)
+    else:
+        dev = svm.svm_device(inst, grid=a.grid)
+        D = inst.max_norm
+        spec = meta.OracleSpec(dev.cone, 2 * D, w["d"] + 2, dev, 2.0, meta.Orientation.MIN,
+                               counter_progress=True)
+        alpha = 0.3
+    print(f"upload {time.time()-t0:.2f}s info {json.dumps(dev.handle.info())}", flush=True)
+    st = meta.EarlyStopConfig(enabled=False)
+    bytes_pass = bench.alg_bytes_per_pass(w)
+    for rep in range(3):
+        r = meta.refine_run(spec, alpha, a.horizon, st, dev.progress)
+        us = r.kernel_ms * 1e3 / max(r.passes, 1)
+        print(f"refine h={a.horizon}: {type(r).__name__} iters {r.iterations} passes {r.passes} "
+              f"kernel {r.kernel_ms:.1f} ms -> {us:.2f} us/pass, "
+              f"{bytes_pass / us / 1e3:.1f} GB/s", flush=True)
+    if a.full:
+        dev.close()
+        t0 = time.time()
+        rep, sol = bench.solve(w, inst, None)
+        print(f"full solve {time.time()-t0:.1f}s iters {rep.total_iterations} steps "
+              f"{rep.search_steps} {rep.termination.value} kernel {rep.kernel_ms/1e3:.1f}s "
+              f"passes {rep.passes} result "
+              f"{sol.radius if w['kind']=='ses' else sol.margin}", flush=True)
+        for s in rep.steps:
+            print("  ", s, flush=True)
+
+
+if __name__ == "__main__":
+    main()
