@@ -93,37 +93,39 @@ __global__ void colsum_kernel(const double* X, int64_t a, int64_t b, int d, int 
 using namespace scmwu;
 
 struct LaunchCfg {
-    int lpr, cpl;
+    int lpr, cpl, nb;
 };
 
 static bool pick_cfg(int d, LaunchCfg& c) {
-    static const int tab[][3] = {{4, 2, 2},    {8, 2, 4},    {12, 4, 3},   {16, 4, 4},
-                                 {24, 4, 6},   {32, 4, 8},   {48, 8, 6},   {64, 8, 8},
-                                 {80, 8, 10},  {104, 8, 13}, {128, 8, 16}, {192, 16, 12},
-                                 {256, 16, 16}, {384, 32, 12}, {512, 32, 16}};
+    // {max d, lanes per row, columns per lane, row-groups per batch}
+    static const int tab[][4] = {{4, 2, 2, 2},     {8, 2, 4, 2},     {12, 4, 3, 4},
+                                 {16, 4, 4, 4},    {24, 4, 6, 4},    {32, 4, 8, 4},
+                                 {48, 8, 6, 4},    {64, 8, 8, 4},    {80, 8, 10, 4},
+                                 {104, 8, 13, 4},  {128, 8, 16, 2},  {192, 16, 12, 2},
+                                 {256, 16, 16, 2}, {384, 32, 12, 2}, {512, 32, 16, 2}};
     for (auto& r : tab)
-        if (d <= r[0]) { c.lpr = r[1]; c.cpl = r[2]; return true; }
+        if (d <= r[0]) { c.lpr = r[1]; c.cpl = r[2]; c.nb = r[3]; return true; }
     return false;
 }
 
 // kernels are instantiated in scmwu_inst_*.cu (compiled in parallel)
 namespace scmwu {
-KernelFn scmwu_lookup_0(int kind, int lpr, int cpl);
-KernelFn scmwu_lookup_1(int kind, int lpr, int cpl);
-KernelFn scmwu_lookup_2(int kind, int lpr, int cpl);
-KernelFn scmwu_lookup_3(int kind, int lpr, int cpl);
-KernelFn scmwu_lookup_4(int kind, int lpr, int cpl);
-KernelFn scmwu_lookup_5(int kind, int lpr, int cpl);
-KernelFn scmwu_lookup_6(int kind, int lpr, int cpl);
-KernelFn scmwu_lookup_7(int kind, int lpr, int cpl);
+KernelFn scmwu_lookup_0(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_1(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_2(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_3(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_4(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_5(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_6(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_7(int kind, int lpr, int cpl, int nb);
 }  // namespace scmwu
 
-static KernelFn kernel_lookup(int kind, int lpr, int cpl) {
-    KernelFn (*fns[])(int, int, int) = {scmwu_lookup_0, scmwu_lookup_1, scmwu_lookup_2,
+static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb) {
+    KernelFn (*fns[])(int, int, int, int) = {scmwu_lookup_0, scmwu_lookup_1, scmwu_lookup_2,
                                         scmwu_lookup_3, scmwu_lookup_4, scmwu_lookup_5,
                                         scmwu_lookup_6, scmwu_lookup_7};
     for (auto f : fns)
-        if (KernelFn k = f(kind, lpr, cpl)) return k;
+        if (KernelFn k = f(kind, lpr, cpl, nb)) return k;
     return nullptr;
 }
 
@@ -192,11 +194,9 @@ static int configure(sc_handle* h, int grid_req) {
         for (int b = gP; b <= G; ++b) rb[b] = n1 + (int64_t)((__int128)n2 * (b - gP) / (G - gP));
         h->gP = gP;
     }
-    // tiles: a multiple of the warp-step, about 24-48 KB
+    // warp tiles: NB row-groups of RPW rows; one SW-stage ring per consumer warp
     const int64_t rowb = (int64_t)h->ld * 8;
-    int m = (int)std::max<int64_t>(1, (32 * 1024) / (step * rowb));
-    int tr = (int)(step * m);
-    if ((int64_t)tr * rowb > 48 * 1024 && m > 1) tr = (int)(step * (m - 1));
+    const int tr = h->cfg.nb * RPW;
     h->tile_rows = tr;
     const uint32_t xb = (uint32_t)((int64_t)tr * rowb);
     h->rad_off = (xb + 15) & ~15u;
@@ -204,18 +204,19 @@ static int configure(sc_handle* h, int grid_req) {
     h->stage_stride = (h->rad_off + radb + 127) & ~127u;
     int64_t max_rows = 0;
     for (int b = 0; b < G; ++b) max_rows = std::max(max_rows, rb[b + 1] - rb[b]);
-    const int tiles = (int)((max_rows + tr - 1) / tr);
-    // stages: fill the remaining shared memory
-    int S = 2;
-    for (;;) {
-        size_t need = (size_t)(S + 1) * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, S + 1);
-        if (need > (size_t)kMaxSmem || S + 1 > 64) break;
-        ++S;
-    }
-    h->resident = tiles <= S ? 1 : 0;
-    if (h->resident) S = std::max(tiles, 1);
+    const int nwt = (int)((max_rows + tr - 1) / tr);
+    const int per_warp = (nwt + kNW - 1) / kNW;
+    auto need = [&](int sw) {
+        return (size_t)kNW * sw * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, kNW * sw);
+    };
+    (void)0;
+    int S = 1;
+    while (S < 64 && need(S + 1) <= (size_t)kMaxSmem) ++S;
+    h->resident = per_warp <= S ? 1 : 0;
+    if (h->resident) S = std::max(per_warp, 1);
+    else if (S < 2) { h->err = "shared memory too small for a double-buffered ring"; return SC_EARG; }
     h->stages = S;
-    h->smem = (size_t)S * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, S);
+    h->smem = need(S);
     if (h->smem > (size_t)kMaxSmem) { h->err = "shared memory budget exceeded"; return SC_EARG; }
     h->grid = G;
     if (h->row_begin) cudaFree(h->row_begin);
@@ -251,7 +252,7 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail, con
     const int d = prob->d;
     const int64_t n = prob->n;
     if (!pick_cfg(d, h->cfg)) { h->err = "d > 512 is not supported yet"; return SC_EARG; }
-    h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl);
+    h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl, h->cfg.nb);
     if (!h->fn) { h->err = "no kernel instantiated for this d"; return SC_EARG; }
     h->dd = prob->kind == SC_SES ? d + 1 : d + 2;
     h->ld = (d + 1) & ~1;
@@ -506,6 +507,7 @@ int sc_info(const sc_handle* h, int64_t* out) {
     if (!h || !out) return SC_EARG;
     out[0] = h->grid; out[1] = kThreads; out[2] = h->cfg.lpr; out[3] = h->cfg.cpl;
     out[4] = h->tile_rows; out[5] = h->stages; out[6] = h->resident; out[7] = (int64_t)h->smem;
+    (void)h->cfg.nb;
     return SC_OK;
 }
 

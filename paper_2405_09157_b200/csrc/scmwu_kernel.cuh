@@ -4,15 +4,18 @@
 // per SM (grid G <= 148).  Every MWU iteration is ONE streaming pass over the
 // point matrix X (n x d fp64, row-sharded across CTAs):
 //
-//   producer warp   cp.async.bulk (1-D TMA) of X tiles (+ radii) into an
-//                   S-stage shared-memory ring, mbarrier full/empty handshake;
-//                   it keeps prefetching the next pass while the consumers sit
-//                   in the grid reduction and the control tail, so HBM never idles.
-//   consumer warps  lane groups of LPR lanes own one row each; CPL columns per
-//                   lane live in registers.  Per row: the closed-form cone
-//                   exponential (2 exp for SES, 1 for SVM), the oracle sums and
-//                   every deferred check.  Partials are reduced
-//                   warp -> CTA -> global (fixed order, deterministic).
+//   streaming       every warp owns every 8th warp tile (TRW rows + radii) of its
+//                   CTA's rows and keeps SW of them in flight in its own shared-
+//                   memory ring: lane 0 issues cp.async.bulk (1-D TMA) copies that
+//                   complete on per-stage mbarriers; the stream wraps into the next
+//                   pass, so those copies land during the grid reduction and tail.
+//   compute         lane groups of LPR lanes own one row, CPL columns per lane in
+//                   registers; NB row-groups are reduced together by a shuffle
+//                   reduce-scatter so every lane then runs the per-row scalar math
+//                   (closed-form cone exponential: 2 exp for SES, 1 for SVM) for its
+//                   own row; a second sweep over the staged rows accumulates the
+//                   weighted d-vector.  Every deferred check rides along
+//                   (DESIGN.md §3-4).  Partials: warp -> CTA -> global, fixed order.
 //   grid reduction  partials[G][RW] in HBM/L2, barrier, column-distributed fold,
 //                   barrier, every CTA reads the RW reduced values.
 //   control tail    warp 0 of every CTA runs scmwu_control.h redundantly (same
@@ -40,8 +43,8 @@
 
 namespace scmwu {
 
-constexpr int kNW = 7;                      // consumer warps (8 warps total: 255 regs)
-constexpr int kThreads = (kNW + 1) * 32;    // + 1 producer warp
+constexpr int kNW = 8;                      // warps per CTA; each streams its own tiles
+constexpr int kThreads = kNW * 32;          // 256 threads: up to 255 registers
 constexpr int kNumSlots = 5;                // pending, callmin, sep, best, last
 constexpr double kInvSqrt2 = 0.7071067811865476;
 constexpr int kMaxSmem = 232448;            // 227 KB opt-in per CTA on sm_100
@@ -87,7 +90,7 @@ struct WarpLanes {
 struct KParams {
     int kind, d, ld, dd, rw, pw;
     int G, gP;                 // grid; SVM: CTAs [0, gP) hold P rows
-    int tile_rows, stages, resident;
+    int tile_rows, stages, resident;   // rows per warp tile, stages per warp ring
     int64_t n, n1;
     const double* X;           // n x ld (ld even, padded with zeros)
     const double* radii;       // SES: n rounded up to even (zero padded)
@@ -252,38 +255,41 @@ __device__ __forceinline__ double across_min(double x) {
 
 // --------------------------------------------------------------------------------------
 // shared-memory map
+//
+// ring: kNW per-warp rings of SW stages; stage (w, s) holds TRW rows of X (+ radii).
 struct SmemMap {
-    uint64_t* full;
-    uint64_t* empty;
+    uint64_t* full;    // [kNW * SW]
+    uint64_t* empty;   // [kNW * SW]
     double* vec;       // 10 control vectors of dd8
     double* ytd;       // y_tilde dummy for CTAs != 0
     double* red;       // rw
     double* wpart;     // kNW x pw
     PassParams* pp;
     sc_ftp_result* resd;
-    volatile int* flags;  // [0] done, [1] consumed tiles
+    volatile int* flags;  // spare
     unsigned char* ring;
 };
 
 __host__ __device__ inline int dd8_of(int dd) { return (dd + 1) & ~1; }
 
-__host__ __device__ inline size_t smem_fixed_bytes(int dd, int rw, int pw, int stages) {
+__host__ __device__ inline size_t smem_fixed_bytes(int dd, int rw, int pw, int nstages) {
     size_t b = 0;
-    b += 2 * (size_t)stages * 8;                       // mbarriers
+    b += 2 * (size_t)nstages * 8;                      // mbarriers
     b += 11 * (size_t)dd8_of(dd) * 8;                  // control vectors + y_tilde dummy
     b += (size_t)((rw + 1) & ~1) * 8;                  // red
     b += (size_t)kNW * ((pw + 1) & ~1) * 8;            // warp partials
-    b += sizeof(PassParams) + sizeof(sc_ftp_result) + 64;
+    b += sizeof(PassParams) + sizeof(sc_ftp_result) + 16 * 4 + 64;
     return (b + 127) & ~(size_t)127;
 }
 
 __device__ inline SmemMap carve(unsigned char* base, const KParams& p) {
     SmemMap m;
     m.ring = base;
-    size_t off = (size_t)p.stages * p.stage_stride;
+    const int ns = kNW * p.stages;
+    size_t off = (size_t)ns * p.stage_stride;
     m.full = reinterpret_cast<uint64_t*>(base + off);
-    m.empty = m.full + p.stages;
-    off += 2 * (size_t)p.stages * 8;
+    m.empty = m.full + ns;
+    off += 2 * (size_t)ns * 8;
     const int dd8 = dd8_of(p.dd);
     m.vec = reinterpret_cast<double*>(base + off);
     off += 10 * (size_t)dd8 * 8;
@@ -301,160 +307,236 @@ __device__ inline SmemMap carve(unsigned char* base, const KParams& p) {
     return m;
 }
 
+// tiles of one pass: warp tile j (rows [r0 + j*TRW, ...)) belongs to consumer warp j % kNW
+__host__ __device__ inline int warp_tile_count(int nwt, int w) {
+    return nwt > w ? (nwt - w + kNW - 1) / kNW : 0;
+}
+
 // --------------------------------------------------------------------------------------
-// producer: stream this CTA's tiles through the ring, pass after pass
-static __device__ void producer(const KParams& p, const SmemMap& m, int64_t r0, int64_t r1,
-                         int ntiles) {
-    if ((threadIdx.x & 31) != 0) return;
-    const int S = p.stages;
-    int64_t issued = 0;
-    auto issue = [&](int64_t seq) {
-        const int stage = (int)(seq % S);
-        const int tile = (int)(seq % ntiles);
-        const int64_t a = r0 + (int64_t)tile * p.tile_rows;
-        const int64_t b = min(r1, a + (int64_t)p.tile_rows);
-        unsigned char* dst = m.ring + (size_t)stage * p.stage_stride;
-        const uint32_t xb = (uint32_t)((b - a) * p.ld * 8);
-        uint32_t bytes = xb;
-        int64_t ra = 0, rb = 0;
-        if (p.kind == SC_SES) {
-            ra = a & ~(int64_t)1;
-            rb = (b + 1) & ~(int64_t)1;
-            bytes += (uint32_t)((rb - ra) * 8);
-        }
-        mbar_arrive_tx(&m.full[stage], bytes);
-        bulk_g2s(dst, p.X + a * p.ld, xb, &m.full[stage]);
-        if (p.kind == SC_SES)
-            bulk_g2s(dst + p.rad_off, p.radii + ra, (uint32_t)((rb - ra) * 8), &m.full[stage]);
-    };
+// per-warp streaming: every warp owns warp tiles j = w, w + kNW, ... of its CTA's rows and
+// keeps SW of them in flight in its own ring (lane 0 issues the bulk copies), so there
+// is no producer bottleneck and no cross-warp coupling.  The stream wraps from pass to
+// pass, so the first SW tiles of the next pass load while the grid reduction and the
+// control tail run.
+struct WarpStream {
+    int cnt;          // warp tiles per pass
+    int q_next;       // local index of the next tile to issue
+    int s;            // stage of the next tile to consume
+    uint32_t phase;   // parity of that stage's full barrier
+    int s_issue;      // stage the next copy goes to (tiles fill stages cyclically)
+    int pending;      // tiles in flight (constant while streaming)
+};
+
+__device__ __forceinline__ void issue_tile(const KParams& p, const SmemMap& m, int64_t r0,
+                                           int64_t r1, int w, int q, int stage) {
+    const int slot = w * p.stages + stage;
+    const int64_t a = r0 + (int64_t)(w + q * kNW) * p.tile_rows;
+    const int64_t b = min(r1, a + (int64_t)p.tile_rows);
+    unsigned char* dst = m.ring + (size_t)slot * p.stage_stride;
+    const uint32_t xb = (uint32_t)((b - a) * p.ld * 8);
+    uint32_t bytes = xb;
+    int64_t ra = 0, rb = 0;
+    if (p.kind == SC_SES) {
+        ra = a & ~(int64_t)1;
+        rb = (b + 1) & ~(int64_t)1;
+        bytes += (uint32_t)((rb - ra) * 8);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(&m.full[slot], bytes);
+    bulk_g2s(dst, p.X + a * p.ld, xb, &m.full[slot]);
+    if (p.kind == SC_SES)
+        bulk_g2s(dst + p.rad_off, p.radii + ra, (uint32_t)((rb - ra) * 8), &m.full[slot]);
+}
+
+__device__ __forceinline__ void stream_start(const KParams& p, const SmemMap& m, int64_t r0,
+                                             int64_t r1, int w, WarpStream& ws, int nwt) {
+    ws.cnt = warp_tile_count(nwt, w);
+    ws.s = 0;
+    ws.phase = 0;
+    const int first = ws.cnt < p.stages ? ws.cnt : p.stages;
+    if ((threadIdx.x & 31) == 0)
+        for (int q = 0; q < first; ++q) issue_tile(p, m, r0, r1, w, q, q);
+    ws.pending = first;
+    ws.s_issue = first % p.stages;
+    ws.q_next = ws.cnt > 0 ? first % ws.cnt : 0;
+}
+
+__device__ __forceinline__ const unsigned char* acquire_stage(const KParams& p,
+                                                              const SmemMap& m, int w,
+                                                              const WarpStream& ws,
+                                                              int pass_idx) {
+    const int slot = w * p.stages + ws.s;
+    if (!p.resident || pass_idx == 0) mbar_wait(&m.full[slot], ws.phase);
+    return m.ring + (size_t)slot * p.stage_stride;
+}
+
+// after the warp finished reading the stage: refill it with the tile SW ahead
+__device__ __forceinline__ void release_stage(const KParams& p, const SmemMap& m, int64_t r0,
+                                              int64_t r1, int w, WarpStream& ws) {
     if (p.resident) {
-        for (int64_t s = 0; s < ntiles; ++s) issue(s);
-        issued = ntiles;
-    } else {
-        for (;;) {
-            const int stage = (int)(issued % S);
-            const int64_t k = issued / S;
-            bool quit = false;
-            if (k > 0) {
-                const uint32_t par = (uint32_t)((k - 1) & 1);
-                while (!mbar_try_wait(&m.empty[stage], par)) {
-                    if (m.flags[0]) { quit = true; break; }
-                }
-            }
-            if (quit || m.flags[0]) break;
-            issue(issued);
-            ++issued;
-        }
+        ws.s = ws.s + 1 == ws.cnt ? 0 : ws.s + 1;
+        return;
     }
-    // wait for the completion of every copy still in flight before the CTA exits
-    while (!m.flags[0]) {
-    }
-    __threadfence_block();
-    const int64_t consumed = p.resident ? 0 : (int64_t)m.flags[1];
-    for (int64_t s = consumed; s < issued; ++s) {
-        const int stage = (int)(s % S);
-        mbar_wait(&m.full[stage], (uint32_t)((s / S) & 1));
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, w, ws.q_next, ws.s_issue);
+    ws.q_next = ws.q_next + 1 == ws.cnt ? 0 : ws.q_next + 1;
+    ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
+    if (++ws.s == p.stages) { ws.s = 0; ws.phase ^= 1u; }
+}
+
+// before exit: the SW copies of the next pass are still in flight
+__device__ __forceinline__ void stream_drain(const KParams& p, const SmemMap& m, int w,
+                                             WarpStream& ws) {
+    if (p.resident) return;
+    for (int i = 0; i < ws.pending; ++i) {
+        mbar_wait(&m.full[w * p.stages + ws.s], ws.phase);
+        if (++ws.s == p.stages) { ws.s = 0; ws.phase ^= 1u; }
     }
 }
 
 // --------------------------------------------------------------------------------------
-// consumer pass over this CTA's rows: SES
-template <int LPR, int CPL, bool CHECK>
+// batched row math: NB row-groups of RPW rows are reduced by a shuffle reduce-scatter,
+// after which lane (grp, l) holds the complete sums of row (l / DUP) * RPW + grp
+// (DUP = LPR / NB identical copies), so the per-row scalar math (sqrt, exp, div) runs
+// once per lane for NB * RPW rows instead of once per lane group.
+template <int LPR, int NB, int V>
+__device__ __forceinline__ void reduce_scatter(double (&v)[V][NB], int l) {
+#pragma unroll
+    for (int lev = 0, o = LPR / 2, half = NB / 2; half >= 1; ++lev, o >>= 1, half >>= 1) {
+        const bool up = (l & o) != 0;
+#pragma unroll
+        for (int s = 0; s < V; ++s) {
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+                const double send = up ? v[s][i] : v[s][i + half];
+                const double keep = up ? v[s][i + half] : v[s][i];
+                v[s][i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = LPR / (2 * NB); o >= 1; o >>= 1) {
+#pragma unroll
+        for (int s = 0; s < V; ++s) v[s][0] += __shfl_xor_sync(0xffffffffu, v[s][0], o);
+    }
+}
+
+// --------------------------------------------------------------------------------------
+// consumer pass over this warp's tiles: SES
+template <int LPR, int CPL, int NB, bool CHECK>
 __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& pp,
-                         int64_t r0, int64_t r1, int ntiles, int64_t& consumed, int pass_idx) {
+                         int64_t r0, int64_t r1, WarpStream& ws, int pass_idx) {
     constexpr int RPW = 32 / LPR;
+    constexpr int DUP = LPR / NB;
+    constexpr int NV = CHECK ? 4 : 3;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
     const int d = p.d, ld = p.ld, dd8 = dd8_of(p.dd);
     const double* ysum = m.vec;
     const double* yprev = m.vec + dd8;
     const double* ywin = m.vec + 5 * dd8;
-    double U[CPL], up[CPL], Sd[CPL];
+    bool ok[CPL];
+    double U[CPL], up[CPL], yw[CPL], Sd[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int j = l + LPR * c;
-        U[c] = j < d ? ysum[j] : 0.0;
-        up[c] = j < d ? yprev[j] : 0.0;
+        ok[c] = j < d;
+        U[c] = ok[c] ? ysum[j] : 0.0;
+        up[c] = ok[c] ? yprev[j] : 0.0;
+        yw[c] = (CHECK && ok[c]) ? ywin[j] : 0.0;
         Sd[c] = 0.0;
     }
     const double t = pp.t, er = pp.eta_rho, al = pp.alpha, sh = pp.shift;
     const double er_t = er * t;
-    double T = 0, Lin = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
     const double inv_t = 1.0 / t;
-    for (int tile = 0; tile < ntiles; ++tile, ++consumed) {
-        const int stage = p.resident ? tile : (int)(consumed % p.stages);
-        if (!p.resident || pass_idx == 0)
-            mbar_wait(&m.full[stage], p.resident ? 0u : (uint32_t)((consumed / p.stages) & 1));
-        const int64_t a = r0 + (int64_t)tile * p.tile_rows;
+    const int myk = l / DUP;                 // row-group whose sums this lane ends up with
+    const bool primary = (l % DUP) == 0;
+    double T = 0, Lin = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
+    for (int q = 0; q < ws.cnt; ++q) {
+        const int j = warp + q * kNW;
+        const unsigned char* st = acquire_stage(p, m, warp, ws, pass_idx);
+        const int64_t a = r0 + (int64_t)j * p.tile_rows;
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
-        const double* xs = reinterpret_cast<const double*>(m.ring + (size_t)stage * p.stage_stride);
-        const double* rs = reinterpret_cast<const double*>(m.ring + (size_t)stage * p.stage_stride +
-                                                           p.rad_off) +
-                           (a & 1);
-        for (int base = warp * RPW; base < nr; base += kNW * RPW) {
-            const int r = base + grp;
-            const bool valid = r < nr;
-            const double* xr = xs + (size_t)(valid ? r : 0) * ld;
-            double df[CPL];
-            double aa = 0, ll = 0, w2 = 0, f2 = 0;
+        const double* xs = reinterpret_cast<const double*>(st);
+        const double* rs = reinterpret_cast<const double*>(st + p.rad_off) + (a & 1);
+        // phase A: per-lane partial sums of NB rows
+        double v[NV][NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            const int r = k * RPW + grp;
+            const double* xr = xs + (size_t)(r < nr ? r : 0) * ld + l;
+            double sa = 0, sl = 0, sw = 0, sf = 0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
-                const int j = l + LPR * c;
-                if (j < d) {
-                    const double v = xr[j];
-                    const double x = fma(-t, v, U[c]);
-                    df[c] = x;
-                    aa = fma(x, x, aa);
-                    ll = fma(v, x, ll);
-                    const double w = up[c] - v;
-                    w2 = fma(w, w, w2);
+                if (ok[c]) {
+                    const double x = xr[LPR * c];
+                    const double df = fma(-t, x, U[c]);
+                    sa = fma(df, df, sa);
+                    sl = fma(x, df, sl);
+                    const double wv = up[c] - x;
+                    sw = fma(wv, wv, sw);
                     if (CHECK) {
-                        const double y = ywin[j] - v;
-                        f2 = fma(y, y, f2);
+                        const double yv = yw[c] - x;
+                        sf = fma(yv, yv, sf);
                     }
-                } else {
-                    df[c] = 0.0;
                 }
             }
-            aa = group_sum<LPR>(aa);
-            ll = group_sum<LPR>(ll);
-            w2 = group_sum<LPR>(w2);
-            if (CHECK) f2 = group_sum<LPR>(f2);
-            double cc = 0.0;
-            if (valid) {
-                const double g = rs[r];
-                const double ra = sqrt(aa);
-                F = fmax(F, ra * inv_t + g);
-                if (CHECK) Fw = fmax(Fw, sqrt(f2) + g);
-                if (a + r > 0) {
-                    const double nrm = er * ra;
-                    const double x0 = -er_t * (al - g);
-                    const double lp = (x0 + nrm) * kInvSqrt2, lm = (x0 - nrm) * kInvSqrt2;
-                    const double A = exp(lp - sh), B = exp(lm - sh);
-                    cc = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
+            v[0][k] = sa; v[1][k] = sl; v[2][k] = sw;
+            if (CHECK) v[NV - 1][k] = sf;
+        }
+        reduce_scatter<LPR, NB, NV>(v, l);
+        // phase B: per-row scalar math, one row per lane (DUP copies)
+        const int r = myk * RPW + grp;
+        double cc = 0.0;
+        if (r < nr) {
+            const double g = rs[r];
+            const double ra = sqrt(v[0][0]);
+            if (primary) {
+                F = fmax(F, fma(ra, inv_t, g));
+                if (CHECK) Fw = fmax(Fw, sqrt(v[NV - 1][0]) + g);
+            }
+            if (a + r > 0) {
+                const double nrm = er * ra;
+                const double x0 = -er_t * (al - g);
+                const double lp = (x0 + nrm) * kInvSqrt2, lm = (x0 - nrm) * kInvSqrt2;
+                const double A = exp(lp - sh), B = exp(lm - sh);
+                cc = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
+                if (primary) {
                     T += A + B;
-                    Lin = fma(cc, ll, Lin);
+                    Lin = fma(cc, v[1][0], Lin);
                     Rad = fma(g, A + B, Rad);
                     M = fmax(M, lp);
-                    Wd = fmax(Wd, (fabs(al - g) + sqrt(w2)) * kInvSqrt2);
+                    Wd = fmax(Wd, (fabs(al - g) + sqrt(v[2][0])) * kInvSqrt2);
                 }
             }
+        }
+        // phase C: S_d += c_i (U - t v_i), diff recomputed from the staged rows
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) Sd[c] = fma(cc, df[c], Sd[c]);
+        for (int k = 0; k < NB; ++k) {
+            const double ck = __shfl_sync(0xffffffffu, cc, grp * LPR + k * DUP);
+            const int rr = k * RPW + grp;
+            const double* xr = xs + (size_t)(rr < nr ? rr : 0) * ld + l;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                if (ok[c]) {
+                    const double df = fma(-t, xr[LPR * c], U[c]);
+                    Sd[c] = fma(ck, df, Sd[c]);
+                }
+            }
         }
-        if (!p.resident) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&m.empty[stage]);
-        }
+        release_stage(p, m, r0, r1, warp, ws);
     }
-    // warp reduction across lane groups (scalars identical inside a group)
-    T = across_sum<LPR>(T);
-    Lin = across_sum<LPR>(Lin);
-    Rad = across_sum<LPR>(Rad);
-    M = across_max<LPR>(M);
-    F = across_max<LPR>(F);
-    Wd = across_max<LPR>(Wd);
-    Fw = across_max<LPR>(Fw);
+    // warp reduction (all 32 lanes; non-primary lanes hold identities)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T += __shfl_xor_sync(0xffffffffu, T, o);
+        Lin += __shfl_xor_sync(0xffffffffu, Lin, o);
+        Rad += __shfl_xor_sync(0xffffffffu, Rad, o);
+        M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+        F = fmax(F, __shfl_xor_sync(0xffffffffu, F, o));
+        Wd = fmax(Wd, __shfl_xor_sync(0xffffffffu, Wd, o));
+        Fw = fmax(Fw, __shfl_xor_sync(0xffffffffu, Fw, o));
+    }
     double* wp = m.wpart + (size_t)warp * ((p.pw + 1) & ~1);
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
@@ -469,11 +551,12 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
 }
 
 // consumer pass: SVM (this CTA holds one side)
-template <int LPR, int CPL, bool CHECK>
+template <int LPR, int CPL, int NB, bool CHECK>
 __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& pp,
-                         int64_t r0, int64_t r1, int ntiles, int64_t& consumed, int pass_idx,
-                         bool isP) {
+                         int64_t r0, int64_t r1, WarpStream& ws, int pass_idx, bool isP) {
     constexpr int RPW = 32 / LPR;
+    constexpr int DUP = LPR / NB;
+    constexpr int NV = CHECK ? 4 : 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
     const int d = p.d, ld = p.ld, dd8 = dd8_of(p.dd);
@@ -481,84 +564,100 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
     const double* yprev = m.vec + dd8;
     const double* ywin = m.vec + 5 * dd8;
     const double* zv = m.vec + 6 * dd8;
-    double W[CPL], wp_[CPL], G[CPL];
+    bool ok[CPL];
+    double W[CPL], wq[CPL], G[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int j = l + LPR * c;
-        W[c] = j < d ? ysum[j] : 0.0;
-        wp_[c] = j < d ? yprev[j] : 0.0;
+        ok[c] = j < d;
+        W[c] = ok[c] ? ysum[j] : 0.0;
+        wq[c] = ok[c] ? yprev[j] : 0.0;
         G[c] = 0.0;
     }
     const double sg = isP ? 1.0 : -1.0;
     const double S = isP ? pp.S1 : pp.S2;
     const double sp = isP ? pp.s1p : pp.s2p;
     const double er = pp.eta_rho, sh = pp.shift;
+    const int myk = l / DUP;
+    const bool primary = (l % DUP) == 0;
     double T = 0, M = -INFINITY, mres = INFINITY, Wd = 0;
     double eW = isP ? INFINITY : -INFINITY, eY = eW, eZ = eW;
-    for (int tile = 0; tile < ntiles; ++tile, ++consumed) {
-        const int stage = p.resident ? tile : (int)(consumed % p.stages);
-        if (!p.resident || pass_idx == 0)
-            mbar_wait(&m.full[stage], p.resident ? 0u : (uint32_t)((consumed / p.stages) & 1));
-        const int64_t a = r0 + (int64_t)tile * p.tile_rows;
+    for (int q = 0; q < ws.cnt; ++q) {
+        const int j = warp + q * kNW;
+        const unsigned char* st = acquire_stage(p, m, warp, ws, pass_idx);
+        const int64_t a = r0 + (int64_t)j * p.tile_rows;
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
-        const double* xs = reinterpret_cast<const double*>(m.ring + (size_t)stage * p.stage_stride);
-        for (int base = warp * RPW; base < nr; base += kNW * RPW) {
-            const int r = base + grp;
-            const bool valid = r < nr;
-            const double* xr = xs + (size_t)(valid ? r : 0) * ld;
-            double xv[CPL];
+        const double* xs = reinterpret_cast<const double*>(st);
+        double v[NV][NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            const int r = k * RPW + grp;
+            const double* xr = xs + (size_t)(r < nr ? r : 0) * ld + l;
             double dW = 0, dw = 0, dy = 0, dz = 0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
-                const int j = l + LPR * c;
-                const double x = j < d ? xr[j] : 0.0;
-                xv[c] = x;
-                dW = fma(x, W[c], dW);
-                dw = fma(x, wp_[c], dw);
-                if (CHECK && j < d) {
-                    dy = fma(x, ywin[j], dy);
-                    dz = fma(x, zv[j], dz);
+                if (ok[c]) {
+                    const double x = xr[LPR * c];
+                    dW = fma(x, W[c], dW);
+                    dw = fma(x, wq[c], dw);
+                    if (CHECK) {
+                        const int jj = l + LPR * c;
+                        dy = fma(x, ywin[jj], dy);
+                        dz = fma(x, zv[jj], dz);
+                    }
                 }
             }
-            dW = group_sum<LPR>(dW);
-            dw = group_sum<LPR>(dw);
-            if (CHECK) {
-                dy = group_sum<LPR>(dy);
-                dz = group_sum<LPR>(dz);
-            }
-            double e = 0.0;
-            if (valid) {
-                const double lg = -er * (sg * dW - S);
-                e = exp(lg - sh);
+            v[0][k] = dW; v[1][k] = dw;
+            if (CHECK) { v[2][k] = dy; v[3][k] = dz; }
+        }
+        reduce_scatter<LPR, NB, NV>(v, l);
+        const int r = myk * RPW + grp;
+        double e = 0.0;
+        if (r < nr) {
+            const double dW = v[0][0];
+            const double lg = -er * (sg * dW - S);
+            e = exp(lg - sh);
+            if (primary) {
                 T += e;
                 M = fmax(M, lg);
-                const double res = sg * dw - sp;
+                const double res = sg * v[1][0] - sp;
                 Wd = fmax(Wd, fabs(res));
                 mres = fmin(mres, res);
                 if (isP) {
                     eW = fmin(eW, dW);
-                    if (CHECK) { eY = fmin(eY, dy); eZ = fmin(eZ, dz); }
+                    if (CHECK) { eY = fmin(eY, v[2][0]); eZ = fmin(eZ, v[3][0]); }
                 } else {
                     eW = fmax(eW, dW);
-                    if (CHECK) { eY = fmax(eY, dy); eZ = fmax(eZ, dz); }
+                    if (CHECK) { eY = fmax(eY, v[2][0]); eZ = fmax(eZ, v[3][0]); }
                 }
             }
+        }
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) G[c] = fma(e, xv[c], G[c]);
+        for (int k = 0; k < NB; ++k) {
+            const double ek = __shfl_sync(0xffffffffu, e, grp * LPR + k * DUP);
+            const int rr = k * RPW + grp;
+            const double* xr = xs + (size_t)(rr < nr ? rr : 0) * ld + l;
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+                if (ok[c]) G[c] = fma(ek, xr[LPR * c], G[c]);
         }
-        if (!p.resident) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&m.empty[stage]);
-        }
+        release_stage(p, m, r0, r1, warp, ws);
     }
-    T = across_sum<LPR>(T);
-    M = across_max<LPR>(M);
-    mres = across_min<LPR>(mres);
-    Wd = across_max<LPR>(Wd);
-    if (isP) {
-        eW = across_min<LPR>(eW); eY = across_min<LPR>(eY); eZ = across_min<LPR>(eZ);
-    } else {
-        eW = across_max<LPR>(eW); eY = across_max<LPR>(eY); eZ = across_max<LPR>(eZ);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T += __shfl_xor_sync(0xffffffffu, T, o);
+        M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+        mres = fmin(mres, __shfl_xor_sync(0xffffffffu, mres, o));
+        Wd = fmax(Wd, __shfl_xor_sync(0xffffffffu, Wd, o));
+        if (isP) {
+            eW = fmin(eW, __shfl_xor_sync(0xffffffffu, eW, o));
+            eY = fmin(eY, __shfl_xor_sync(0xffffffffu, eY, o));
+            eZ = fmin(eZ, __shfl_xor_sync(0xffffffffu, eZ, o));
+        } else {
+            eW = fmax(eW, __shfl_xor_sync(0xffffffffu, eW, o));
+            eY = fmax(eY, __shfl_xor_sync(0xffffffffu, eY, o));
+            eZ = fmax(eZ, __shfl_xor_sync(0xffffffffu, eZ, o));
+        }
     }
     double* wpp = m.wpart + (size_t)warp * ((p.pw + 1) & ~1);
 #pragma unroll
@@ -575,32 +674,22 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
 
 // --------------------------------------------------------------------------------------
 // the persistent kernel
-template <int KIND, int LPR, int CPL>
+template <int KIND, int LPR, int CPL, int NB>
 __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemMap m = carve(smem, p);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x;
     const int64_t r0 = p.row_begin[b], r1 = p.row_begin[b + 1];
-    const int ntiles = (int)((r1 - r0 + p.tile_rows - 1) / p.tile_rows);
+    const int nwt = (int)((r1 - r0 + p.tile_rows - 1) / p.tile_rows);
     const bool isP = KIND == SC_SVM && b < p.gP;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < p.stages; ++s) {
-            mbar_init(&m.full[s], 1);
-            mbar_init(&m.empty[s], kNW);
-        }
-        m.flags[0] = 0;
-        m.flags[1] = 0;
+        for (int s = 0; s < kNW * p.stages; ++s) mbar_init(&m.full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-
-    if (warp == kNW) {
-        if (ntiles > 0) producer(p, m, r0, r1, ntiles);
-        else if (lane == 0) { while (!m.flags[0]) { } }
-        __syncthreads();
-        return;
-    }
+    WarpStream ws;
+    stream_start(p, m, r0, r1, warp, ws, nwt);
 
     // ------------------------------------------------------------ consumers
     const int dd8 = dd8_of(p.dd);
@@ -630,44 +719,40 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
     }
     consumer_sync();
 
-    int64_t consumed = 0;
     int pass_idx = 0;
     unsigned long long nbar = 0;
     // columns of the reduced vector folded by this CTA
     const int c0 = (int)((int64_t)b * p.rw / p.G), c1 = (int)((int64_t)(b + 1) * p.rw / p.G);
+    const int pws = (p.pw + 1) & ~1;
     while (pp->action == kPass) {
         const PassParams ps = *pp;
-        if (ntiles > 0) {
-            if (KIND == SC_SES) {
-                if (ps.check) ses_pass<LPR, CPL, true>(p, m, ps, r0, r1, ntiles, consumed, pass_idx);
-                else ses_pass<LPR, CPL, false>(p, m, ps, r0, r1, ntiles, consumed, pass_idx);
-            } else {
-                if (ps.check)
-                    svm_pass<LPR, CPL, true>(p, m, ps, r0, r1, ntiles, consumed, pass_idx, isP);
-                else
-                    svm_pass<LPR, CPL, false>(p, m, ps, r0, r1, ntiles, consumed, pass_idx, isP);
-            }
+        if (KIND == SC_SES) {
+            if (ps.check) ses_pass<LPR, CPL, NB, true>(p, m, ps, r0, r1, ws, pass_idx);
+            else ses_pass<LPR, CPL, NB, false>(p, m, ps, r0, r1, ws, pass_idx);
+        } else {
+            if (ps.check) svm_pass<LPR, CPL, NB, true>(p, m, ps, r0, r1, ws, pass_idx, isP);
+            else svm_pass<LPR, CPL, NB, false>(p, m, ps, r0, r1, ws, pass_idx, isP);
         }
         consumer_sync();
         // CTA partial, fixed warp order, written in the reduced layout
-        const int pws = (p.pw + 1) & ~1;
+        const int nw_act = nwt < kNW ? nwt : kNW;   // warps that own at least one tile
         for (int j = tid; j < p.rw; j += kNW * 32) {
             double v;
             if (KIND == SC_SES) {
                 const int op = red_op(KIND, j);
                 v = op_identity(op);
-                if (ntiles > 0)
-                    for (int w = 0; w < kNW; ++w) v = op_apply(op, v, m.wpart[w * pws + j]);
+                for (int w = 0; w < nw_act; ++w) v = op_apply(op, v, m.wpart[w * pws + j]);
             } else {
                 int pc, side;
                 svm_src(p.d, j, pc, side);
                 const int op = red_op(KIND, j);
                 v = op_identity(op);
                 const bool mine = side == 0 || (side == 1) == isP;
-                if (mine && ntiles > 0) {
+                if (mine && nw_act > 0) {
                     const int pop = svm_part_op(pc, isP);
                     double acc = op_identity(pop);
-                    for (int w = 0; w < kNW; ++w) acc = op_apply(pop, acc, m.wpart[w * pws + pc]);
+                    for (int w = 0; w < nw_act; ++w)
+                        acc = op_apply(pop, acc, m.wpart[w * pws + pc]);
                     v = acc;
                 }
             }
@@ -695,12 +780,8 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
         consumer_sync();
         ++pass_idx;
     }
-    // stop the producer, then publish the result (CTA 0)
-    if (tid == 0) {
-        m.flags[1] = (int)consumed;
-        __threadfence_block();
-        m.flags[0] = 1;
-    }
+    // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
+    stream_drain(p, m, warp, ws);
     if (b == 0 && warp == 0) {
         for (int j = lane; j < p.dd; j += 32) p.best_y[j] = ctl.v.besty[j];
         if (lane == 0) {
@@ -716,7 +797,7 @@ typedef void (*KernelFn)(const KParams);
 }  // namespace scmwu
 
 // explicit instantiation + lookup, used by the scmwu_inst_*.cu translation units
-#define SCMWU_INST(K, L, C)                                                            \
-    template __global__ void scmwu::scmwu_kernel<K, L, C>(const scmwu::KParams);
-#define SCMWU_MATCH(K, L, C) \
-    if (kind == K && lpr == L && cpl == C) return scmwu::scmwu_kernel<K, L, C>;
+#define SCMWU_INST(K, L, C, B)                                                          \
+    template __global__ void scmwu::scmwu_kernel<K, L, C, B>(const scmwu::KParams);
+#define SCMWU_MATCH(K, L, C, B) \
+    if (kind == K && lpr == L && cpl == C && nb == B) return scmwu::scmwu_kernel<K, L, C, B>;
