@@ -48,7 +48,7 @@ WORKLOADS = {
 }
 # GPU iteration counts of full solves measured by this bench (profiles/); used only by the
 # reference arm to extrapolate the CPU port's s/iter to a time-to-eps.
-ITERS_EST = {"ses_c2": 360_000, "svm_c3": 300_000, "ses_c1": 82_518, "ses_c4": 360_000}
+ITERS_EST = {"ses_c2": 15_515, "svm_c3": 300_000, "ses_c1": 82_518, "ses_c4": 360_000}
 
 
 def make_instance(w):
@@ -127,30 +127,31 @@ def measured_peak():
 
 
 # ------------------------------------------------------------------ CPU (oracle port) sample
-def cpu_sample(w, inst, max_seconds=20.0, max_iters=64):
+def cpu_sample(w, inst, max_seconds=20.0, max_iters=256):
     """Time the oracle port for a bounded number of MWU iterations of the workload:
-    a bracketing-phase feasibility test at the first level the search would try."""
+    one polish run (refine_run, stopping disabled) at the feasible end of the range,
+    which never separates, so exactly `horizon` iterations (>= ceil(ln r)) run."""
     import oracle as O
     t_setup = time.perf_counter()
     if w["kind"] == "ses":
         prob = O.SesProblem(inst.centers, inst.radii)
         D, L0, U0 = prob.range()
         spec = prob.spec(3.0 * D / math.sqrt(2.0))
-        alpha = L0 + (U0 - L0) / 3.0
-        progress = (lambda y: prob.progress(y[:w["d"]]))
+        alpha = U0
     else:
         prob = O.SvmProblem(inst.P, inst.Q)
         spec = prob.spec()
-        alpha = 2.0 * 2.0 * prob.D / 3.0
-        progress = (lambda y: prob.progress(y[:w["d"]]))
+        alpha = 1e-3 * prob.D
+    progress = (lambda y: prob.progress(y[:w["d"]]))
     setup = time.perf_counter() - t_setup
-    # calibrate: 2 iterations, then as many as fit in max_seconds
+    ln_r = math.log(spec.rank)
+    # calibrate on a short run, then as many iterations as fit in max_seconds
     t0 = time.perf_counter()
-    O.ftp(spec, alpha, 0.25, progress=progress, cap=2)
-    per = (time.perf_counter() - t0) / 2.0
-    k = int(max(2, min(max_iters, max_seconds / max(per, 1e-9))))
+    res = O.refine(spec, alpha, 1, 1e-4, 10, False, progress)
+    per = (time.perf_counter() - t0) / res.iterations
+    k = int(max(math.ceil(ln_r), min(max_iters, max_seconds / max(per, 1e-9))))
     t0 = time.perf_counter()
-    res = O.ftp(spec, alpha, 0.25, progress=progress, cap=k)
+    res = O.refine(spec, alpha, k, 1e-4, 10, False, progress)
     dt = time.perf_counter() - t0
     return {"s_per_iter": dt / res.iterations, "iters": res.iterations, "seconds": dt,
             "setup_s": setup}
@@ -177,9 +178,9 @@ def reference_arm(args, w, rank):
         "config": {"workload": w["desc"], "eps": w["eps"], "seed": w["seed"],
                    "extrapolated_from_iters": iters},
         "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "port",
-                         "sample": f"{samples[-1]['iters']} MWU iterations of one feasibility "
-                                   f"test of the workload per step; {spi:.4f} s/iter x "
-                                   f"{iters} iterations (extrapolated)"},
+                         "sample": f"{samples[-1]['iters']} MWU iterations (one refine_run) of "
+                                   f"the workload per step; {spi:.4f} s/iter x {iters} "
+                                   f"iterations (the GPU solve's count; extrapolated)"},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t0,
     }
@@ -296,8 +297,8 @@ def our_arm(args, w, rank, world):
         its = rep0.total_iterations
         line["cpu_baseline"] = {
             "value": s["s_per_iter"] * its, "unit": "s", "cores": 1, "kind": "port",
-            "sample": f"{s['iters']} MWU iterations of the workload's first bracketing test "
-                      f"on the oracle port ({s['s_per_iter']:.4f} s/iter); time-to-eps "
+            "sample": f"{s['iters']} MWU iterations (one refine_run) of the workload on the "
+                      f"oracle port ({s['s_per_iter']:.4f} s/iter); time-to-eps "
                       f"extrapolated x {its} GPU iterations"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -308,7 +309,7 @@ def our_arm(args, w, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ses_c2", choices=sorted(WORKLOADS))
