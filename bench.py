@@ -127,7 +127,7 @@ def measured_peak():
 
 
 # ------------------------------------------------------------------ CPU (oracle port) sample
-def cpu_sample(w, inst, max_seconds=20.0, max_iters=256):
+def cpu_sample(w, inst, max_seconds=20.0, max_iters=100_000):
     """Time the oracle port for a bounded number of MWU iterations of the workload:
     one polish run (refine_run, stopping disabled) at the feasible end of the range,
     which never separates, so exactly `horizon` iterations (>= ceil(ln r)) run."""
@@ -144,15 +144,18 @@ def cpu_sample(w, inst, max_seconds=20.0, max_iters=256):
         alpha = 1e-3 * prob.D
     progress = (lambda y: prob.progress(y[:w["d"]]))
     setup = time.perf_counter() - t_setup
-    ln_r = math.log(spec.rank)
-    # calibrate on a short run, then as many iterations as fit in max_seconds
+    # the shortest run refine_run allows is ceil(ln r) iterations; when that is cheap,
+    # run again with as many iterations as fit in max_seconds
     t0 = time.perf_counter()
     res = O.refine(spec, alpha, 1, 1e-4, 10, False, progress)
-    per = (time.perf_counter() - t0) / res.iterations
-    k = int(max(math.ceil(ln_r), min(max_iters, max_seconds / max(per, 1e-9))))
-    t0 = time.perf_counter()
-    res = O.refine(spec, alpha, k, 1e-4, 10, False, progress)
     dt = time.perf_counter() - t0
+    per = dt / res.iterations
+    if dt < 0.1 * max_seconds:
+        k = int(min(max_iters, max_seconds / max(per, 1e-9)))
+        if k > res.iterations:
+            t0 = time.perf_counter()
+            res = O.refine(spec, alpha, k, 1e-4, 10, False, progress)
+            dt = time.perf_counter() - t0
     return {"s_per_iter": dt / res.iterations, "iters": res.iterations, "seconds": dt,
             "setup_s": setup}
 
@@ -164,7 +167,7 @@ def reference_arm(args, w, rank):
     t0 = time.perf_counter()
     samples = []
     for _ in range(args.warmup):
-        cpu_sample(w, inst, max_seconds=3.0, max_iters=4)
+        cpu_sample(w, inst, max_seconds=3.0, max_iters=1)
     for _ in range(args.steps):
         samples.append(cpu_sample(w, inst, max_seconds=20.0))
     spi = statistics.median(s["s_per_iter"] for s in samples)
