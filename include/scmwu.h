@@ -130,6 +130,10 @@ int sc_mark(sc_handle* h, int32_t which);
 int sc_elapsed(sc_handle* h, float* ms);
 /* Kernel launches issued by this handle since creation (persistent + one-off). */
 int64_t sc_launches(const sc_handle* h);
+/* Diagnostics: with SCMWU_TIMING=1 in the environment, per-phase SM-cycle sums of the
+ * last sc_ftp as seen by CTA 0 (9 values: pass, warp join, CTA partial, barrier 1,
+ * fold, barrier 2, reduced read, control tail, tail join); zeros otherwise. */
+int sc_debug_timing(sc_handle* h, double* out);
 int sc_pd_pair(sc_handle* h, double* mu /* n1 */, double* gam /* n - n1 */, double* dist);
 int sc_set_grid(sc_handle* h, int32_t grid);
 int sc_info(const sc_handle* h, int64_t* out /* 8 values: grid, threads, lanes_per_row,

@@ -65,8 +65,8 @@ class ScFtpResult(ctypes.Structure):
 
 
 EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "sc_pd_pair",
-           "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_last_error",
-           "sc_destroy", "sc_version")
+           "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_debug_timing",
+           "sc_last_error", "sc_destroy", "sc_version")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -106,6 +106,7 @@ class Engine:
         lib.sc_elapsed.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
         lib.sc_launches.argtypes = [vp]
         lib.sc_launches.restype = ctypes.c_int64
+        lib.sc_debug_timing.argtypes = [vp, _dp]
         self.lib = lib
 
     def create(self, kind: int, X, X_tail, radii, D: float, rho: float, R: float,
@@ -214,6 +215,11 @@ class Handle:
         ms = ctypes.c_float()
         self._check(self.engine.lib.sc_elapsed(self.h, ctypes.byref(ms)), "sc_elapsed")
         return float(ms.value)
+
+    def debug_timing(self) -> np.ndarray:
+        out = np.zeros(9)
+        self._check(self.engine.lib.sc_debug_timing(self.h, _ptr(out)), "sc_debug_timing")
+        return out
 
     def launches(self) -> int:
         return int(self.engine.lib.sc_launches(self.h))

@@ -96,8 +96,9 @@ struct CtlVecs {
 
 // Global-memory slots (device) written by the CTA whose `writer` flag is set.
 struct CtlSlots {
-    double* ring;        // window history, ring_cap x dd
+    double* ring;        // window history, ring_cap entries of ring_stride doubles
     int64_t ring_cap;
+    int ring_stride;     // >= dd (even on the device: 16-byte entries for cp.async)
     double* pd_pending;  // SVM: iterate state at the last check  [d+2 | IterState]
     double* pd_callmin;  // SVM: state at the call's smallest counter distance
     double* pd_sep;      // SVM: state of the separating iterate
@@ -147,6 +148,12 @@ struct Control {
 
     CtlVecs v;
     CtlSlots s;
+    // the window entry the next iteration will evict, prefetched into shared memory
+    // while the pass streams (device); nullptr = read it from the ring directly
+    double* evict_buf = nullptr;
+    int64_t evict_idx = -1;
+    // shared-memory copy of the pending pd_counter state (device); nullptr = global
+    double* pend_buf = nullptr;
 
     // ------------------------------------------------------------ helpers
     SC_HD bool is_check(int64_t tt) const {
@@ -162,8 +169,9 @@ struct Control {
     SC_HD void offer_bar(double f) {
         if (!better(f)) return;
         has_best_f = true; best_f = f;
-        const double tt = (double)t;
-        for (int j = L::lane(); j < dd; j += L::nl()) v.besty[j] = v.ysum[j] / tt;
+        const double inv_t = 1.0 / (double)t;
+#pragma unroll 4
+        for (int j = L::lane(); j < dd; j += L::nl()) v.besty[j] = v.ysum[j] * inv_t;
     }
     SC_HD void offer_vec(double f, const double* y) {
         if (!better(f)) return;
@@ -209,6 +217,17 @@ struct Control {
         const int w = dd + (dd & 1) + (int)(sizeof(IterState) / sizeof(double));
         for (int j = L::lane(); j < w; j += L::nl()) dst[j] = L::ldcg(src + j);
     }
+    // shared-memory copy of a state (every CTA keeps it, so commits need no global read)
+    SC_HD void keep_state(double* buf, const double* vec, const IterState& st) {
+        for (int j = L::lane(); j < dd; j += L::nl()) buf[j] = vec[j];
+        if (L::lane() == 0) *reinterpret_cast<IterState*>(buf + dd + (dd & 1)) = st;
+    }
+    SC_HD void store_state(double* slot, const double* buf) {
+        if (!writer) return;
+        const int w = dd + (dd & 1) + (int)(sizeof(IterState) / sizeof(double));
+        L::sync();
+        for (int j = L::lane(); j < w; j += L::nl()) slot[j] = buf[j];
+    }
 
     // ------------------------------------------------------------ results
     SC_HD int finish_primal(double value, int64_t iters) {
@@ -240,6 +259,8 @@ struct Control {
         res->counter_min = has_counter_min ? counter_min : 0.0;
         status = SC_OK;
         save_state(s.last, v.pU, cur);
+        if (evict_idx >= 0) L::prefetch_wait();   // no copy may land after exit
+        evict_idx = -1;
         return kDone;
     }
 
@@ -272,6 +293,8 @@ struct Control {
 
     SC_HD void reset_learner() {
         t = 0; win_head = 0; win_count = 0; win_len = 0;
+        if (evict_idx >= 0) L::prefetch_wait();   // drop a pending prefetch of the old run
+        evict_idx = -1;
         for (int j = L::lane(); j < dd; j += L::nl()) { v.ysum[j] = 0.0; v.wsum[j] = 0.0; }
         shift_pass = 0.0;
     }
@@ -302,7 +325,6 @@ struct Control {
         const int nl = L::nl(), ln = L::lane();
         double value;
         cur.t = (double)t; cur.eta = eta; cur.shift = shift_pass;
-        for (int j = ln; j < dd; j += nl) v.pU[j] = v.ysum[j];
         if (kind == SC_SES) {
             // s = sum_i W_i = -(eta/rho)/T * sum_i c_i (U - t v_i)      (R/ses.py:109-112)
             const double Tt = red[kS_T];
@@ -311,21 +333,22 @@ struct Control {
                 return finish_sep(-INFINITY, k, red, y_tilde);
             }
             const double coef = -(eta * inv_rho) / Tt;
-            double s2 = 0.0;
+            // one reduction for |s|^2 and s.v1: s.u = s.v1 + (alpha - g1) |s|^2 / |s|
+            double s2 = 0.0, sv = 0.0;
+#pragma unroll 4
             for (int j = ln; j < d; j += nl) {
-                double sj = coef * red[kS_Vec + j];
+                const double sj = coef * red[kS_Vec + j];
                 v.ynew[j] = sj;          // temporarily s
-                s2 += sj * sj;
+                s2 = fma(sj, sj, s2);
+                sv = fma(sj, v.v1[j], sv);
             }
-            const double sn = sqrt(L::sum(s2));
-            double su = 0.0;
-            for (int j = ln; j < d; j += nl) {
-                double sj = v.ynew[j];
-                double u = sn > 0.0 ? v.v1[j] + (a.alpha - g1) * (sj / sn) : v.v1[j];
-                su += sj * u;
-                v.ynew[j] = u;
-            }
-            su = L::sum(su);
+            L::sum2(s2, sv);
+            const double sn = sqrt(s2);
+            const double am = a.alpha - g1;
+            const double inv_sn = sn > 0.0 ? 1.0 / sn : 0.0;
+#pragma unroll 4
+            for (int j = ln; j < d; j += nl) v.ynew[j] = fma(am * inv_sn, v.ynew[j], v.v1[j]);
+            const double su = sn > 0.0 ? fma(am * inv_sn, s2, sv) : sv;
             const double lin = coef * red[kS_Lin];
             const double rad = red[kS_Rad] / (kSqrt2 * Tt);
             value = su + a.alpha / kSqrt2 - lin - rad;            // R/ses.py:123
@@ -338,21 +361,21 @@ struct Control {
             const double Tt = TP + TQ;
             cur.T = Tt; cur.TP = TP; cur.TQ = TQ;
             cur.S1 = v.ysum[d]; cur.S2 = v.ysum[d + 1];
+            const double inv_T = 1.0 / Tt;
             double g2 = 0.0;
+#pragma unroll 4
             for (int j = ln; j < d; j += nl) {
-                double gj = (red[kV_Vec + j] - red[kV_Vec + d + j]) / Tt;
+                const double gj = (red[kV_Vec + j] - red[kV_Vec + d + j]) * inv_T;
                 v.ynew[j] = gj;
-                g2 += gj * gj;
+                g2 = fma(gj, gj, g2);
             }
-            const double gn = sqrt(L::sum(g2));
-            double gw = 0.0;
-            for (int j = ln; j < d; j += nl) {
-                double gj = v.ynew[j];
-                double w = gn > 0.0 ? gj / gn : (j == 0 ? 1.0 : 0.0);
-                gw += gj * w;
-                v.ynew[j] = w;
-            }
-            gw = L::sum(gw);
+            g2 = L::sum(g2);
+            const double gn = sqrt(g2);
+            const double inv_gn = gn > 0.0 ? 1.0 / gn : 0.0;
+#pragma unroll 4
+            for (int j = ln; j < d; j += nl)
+                v.ynew[j] = gn > 0.0 ? v.ynew[j] * inv_gn : (j == 0 ? 1.0 : 0.0);
+            const double gw = gn > 0.0 ? g2 * inv_gn : 0.0;       // g . w
             const double tm = TP / Tt, tg = TQ / Tt;
             const double s1 = tm <= tg ? D : a.alpha - D;
             const double s2v = a.alpha - s1;
@@ -363,33 +386,42 @@ struct Control {
                 if (j == d + 1) v.ynew[j] = s2v;
             }
         }
-        L::sync();
-        // ---- accepted witness: y_sum += y; the width check is deferred to the next pass
+        // ---- accepted witness: y_sum += y, window push; the width check of this
+        // iteration is deferred to the next pass
         const bool chk = is_check(k);
         if (kind == SC_SVM && chk) {
             // pd_counter at this iterate (R/svm.py:173-181): z = GP/TP - GQ/TQ
-            const double TP = red[kV_TP], TQ = red[kV_TQ];
+            const double iP = 1.0 / red[kV_TP], iQ = 1.0 / red[kV_TQ];
             double z2 = 0.0;
+#pragma unroll 4
             for (int j = ln; j < d; j += nl) {
-                double z = red[kV_Vec + j] / TP - red[kV_Vec + d + j] / TQ;
+                const double z = red[kV_Vec + j] * iP - red[kV_Vec + d + j] * iQ;
                 v.zv[j] = z;
-                z2 += z * z;
+                z2 = fma(z, z, z2);
             }
             dist_prev = sqrt(L::sum(z2));
-            save_state(s.pd_pending, v.pU, cur);
+            // the state of this iterate (y_sum before the update) for a later commit
+            save_state(s.pd_pending, v.ysum, cur);
+            if (pend_buf != nullptr) keep_state(pend_buf, v.ysum, cur);
         }
+        double* slot = s.ring + (win_count % s.ring_cap) * s.ring_stride;
+#pragma unroll 4
         for (int j = ln; j < dd; j += nl) {
-            double y = v.ynew[j];
+            const double y = v.ynew[j];
+            v.pU[j] = v.ysum[j];
             v.ysum[j] += y;
             v.yprev[j] = y;
+            if (writer) slot[j] = y;
+            v.wsum[j] += y;
         }
         t = k;
         value_prev = value;
         check_prev = chk;
         push_window(k);
         if (chk) {
-            const double len = (double)win_len;
-            for (int j = ln; j < dd; j += nl) v.ywin[j] = v.wsum[j] / len;
+            const double inv_len = 1.0 / (double)win_len;
+#pragma unroll 4
+            for (int j = ln; j < dd; j += nl) v.ywin[j] = v.wsum[j] * inv_len;
         }
         // lagged shift for the next pass: the max eigenvalue / logit of this iterate
         const double m = kind == SC_SES ? red[kS_M] : red[kV_M];
@@ -400,39 +432,50 @@ struct Control {
     }
 
     SC_HD int finish_sep(double value, int64_t k, const double* red, double* y_tilde) {
+        for (int j = L::lane(); j < dd; j += L::nl()) v.pU[j] = v.ysum[j];
         if (kind == SC_SVM) {
-            const double TP = red[kV_TP], TQ = red[kV_TQ];
+            const double iP = 1.0 / red[kV_TP], iQ = 1.0 / red[kV_TQ];
             double z2 = 0.0;
             for (int j = L::lane(); j < d; j += L::nl()) {
-                double z = red[kV_Vec + j] / TP - red[kV_Vec + d + j] / TQ;
-                z2 += z * z;
+                const double z = red[kV_Vec + j] * iP - red[kV_Vec + d + j] * iQ;
+                z2 = fma(z, z, z2);
             }
             res->sep_dist = sqrt(L::sum(z2));
-            save_state(s.pd_sep, v.pU, cur);
+            save_state(s.pd_sep, v.ysum, cur);
         }
         const int64_t iters = a.mode == SC_MODE_FTP ? spent + k : k;
         return finish_primal(value, iters);
     }
 
-    // suffix window (R/meta.py:330-335 / :514-519)
+    // suffix window (R/meta.py:330-335 / :514-519): the new y was added to the
+    // ring and the sum by process_iterate; evict down to max(64, t/2) entries
     SC_HD void push_window(int64_t tt) {
         const int nl = L::nl(), ln = L::lane();
-        double* slot = s.ring + (win_count % s.ring_cap) * dd;
-        for (int j = ln; j < dd; j += nl) {
-            double y = v.ynew[j];
-            if (writer) slot[j] = y;
-            v.wsum[j] += y;
-        }
         ++win_count; ++win_len;
         const int64_t lim = kLadderBase > tt / 2 ? kLadderBase : tt / 2;
         while (win_len > lim) {
-            const double* old = s.ring + (win_head % s.ring_cap) * dd;
-            for (int j = ln; j < dd; j += nl) v.wsum[j] -= L::ldcg(old + j);
+            if (evict_buf != nullptr && win_head == evict_idx) {
+                L::prefetch_wait();
+                for (int j = ln; j < dd; j += nl) v.wsum[j] -= evict_buf[j];
+                evict_idx = -1;
+            } else {
+                const double* old = s.ring + (win_head % s.ring_cap) * s.ring_stride;
+                for (int j = ln; j < dd; j += nl) v.wsum[j] -= L::ldcg(old + j);
+            }
             ++win_head; --win_len;
         }
     }
 
+    // start fetching the entry the next push may evict (it was written >= 64
+    // iterations ago, so it is visible to every CTA)
+    SC_HD void prefetch_eviction() {
+        if (evict_buf == nullptr || win_len < kLadderBase) return;
+        evict_idx = win_head;
+        L::prefetch(evict_buf, s.ring + (win_head % s.ring_cap) * s.ring_stride, s.ring_stride);
+    }
+
     SC_HD void write_pass(PassParams* pp) {
+        prefetch_eviction();
         if (L::lane() != 0) return;
         pp->t = (double)t;
         pp->alpha = a.alpha;
@@ -525,7 +568,8 @@ struct Control {
                 const double cv = dist_prev;
                 if (!has_counter_min || cv < counter_min) {
                     has_counter_min = true; counter_min = cv;
-                    copy_slot(s.pd_callmin, s.pd_pending);
+                    if (pend_buf != nullptr) store_state(s.pd_callmin, pend_buf);
+                    else copy_slot(s.pd_callmin, s.pd_pending);
                 }
                 offer_counter(cv);
                 offer_z(svm_margin(red[kV_minPz], red[kV_maxQz], cv));

@@ -1,5 +1,7 @@
 // scmwu_host.cu — host side of the B200 engine: the C ABI of include/scmwu.h,
 // launch configuration and the one-off kernels (progress, iterate, column sums).
+#include <stdlib.h>
+
 #include "scmwu_kernel.cuh"
 
 namespace scmwu {
@@ -149,6 +151,7 @@ struct sc_handle {
     sc_ftp_result* res = nullptr;
     double *y_tilde = nullptr, *best_y = nullptr, *scratch = nullptr, *yvec = nullptr;
     int* status = nullptr;
+    long long* timing = nullptr;     // SCMWU_TIMING=1: per-phase cycle sums of the last call
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, mk0 = nullptr, mk1 = nullptr;
     int64_t launches = 0;
@@ -354,12 +357,13 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     CK(cudaSetDevice(h->prob.device), "set device");
     // window history: max(64, T/2) + 2 entries (the largest rung is <= T)
     int64_t need = std::max<int64_t>(kLadderBase, T / 2) + 2;
-    const int64_t cap_lim = ((int64_t)1 << 30) / (h->dd * 8);   // 1 GiB
+    const int dd8 = (h->dd + 1) & ~1;                             // 16-byte ring entries
+    const int64_t cap_lim = ((int64_t)1 << 30) / (dd8 * 8);       // 1 GiB
     if (need > cap_lim) need = cap_lim;
     if (need > h->ring_cap) {
         if (h->ring) cudaFree(h->ring);
         h->ring = nullptr;
-        CK(cudaMalloc(&h->ring, (size_t)need * h->dd * 8), "alloc window ring");
+        CK(cudaMalloc(&h->ring, (size_t)need * dd8 * 8), "alloc window ring");
         h->ring_cap = need;
     }
     KParams p;
@@ -367,6 +371,12 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     p.kind = h->prob.kind; p.d = h->prob.d; p.ld = h->ld; p.dd = h->dd; p.rw = h->rw; p.pw = h->pw;
     p.G = h->grid; p.gP = h->gP; p.tile_rows = h->tile_rows; p.stages = h->stages;
     p.resident = h->resident; p.n = h->prob.n; p.n1 = h->prob.n1;
+    // every CTA re-reads all partials when that is cheap (<= 192 KB per CTA)
+    // grid reduction scheme (SCMWU_FOLD=0 two barriers, 1 redundant, 2 last arriver)
+    // measured on B200 (profiles/r01_overhead.md): two barriers 8.3 us/pass at C1,
+    // last-arriver 16.9 us (147 CTAs poll one line while one CTA folds), redundant worse
+    p.fold_mode = kFoldTwoBarriers;
+    if (const char* f = getenv("SCMWU_FOLD")) p.fold_mode = atoi(f);
     p.X = h->X; p.radii = h->radii; p.row_begin = h->row_begin;
     p.rho = h->prob.rho; p.inv_rho = 1.0 / h->prob.rho; p.R = h->prob.R; p.ln_r = h->prob.ln_r;
     p.D = h->prob.D; p.g1 = h->g1;
@@ -375,6 +385,8 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     h->last_alpha = args->alpha;
     p.args = *args; p.res = h->res; p.y_tilde = h->y_tilde; p.best_y = h->best_y;
     p.status = h->status; p.stage_stride = h->stage_stride; p.rad_off = h->rad_off;
+    if (!h->timing && getenv("SCMWU_TIMING")) CK(cudaMalloc(&h->timing, 16 * 8), "alloc timing");
+    p.timing = h->timing;
     CK(cudaMemsetAsync(h->bar, 0, 64, h->stream), "reset barrier");
     CK(cudaMemsetAsync(h->res, 0, sizeof(sc_ftp_result), h->stream), "reset result");
     CK(cudaMemsetAsync(h->status, 0xff, sizeof(int), h->stream), "reset status");
@@ -527,12 +539,21 @@ int sc_elapsed(sc_handle* h, float* ms) {
 
 int64_t sc_launches(const sc_handle* h) { return h ? h->launches : 0; }
 
+int sc_debug_timing(sc_handle* h, double* out) {
+    if (!h || !out) return SC_EARG;
+    if (!h->timing) { for (int i = 0; i < 9; ++i) out[i] = 0.0; return SC_OK; }
+    long long t[9];
+    CK(cudaMemcpy(t, h->timing, sizeof(t), cudaMemcpyDeviceToHost), "copy timing");
+    for (int i = 0; i < 9; ++i) out[i] = (double)t[i];
+    return SC_OK;
+}
+
 const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 void sc_destroy(sc_handle* h) {
     if (!h) return;
     cudaSetDevice(h->prob.device);
-    void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar,
+    void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar, h->timing,
                     h->ring, h->slots, h->res, h->y_tilde, h->best_y, h->scratch, h->yvec,
                     h->status};
     for (void* b : bufs)

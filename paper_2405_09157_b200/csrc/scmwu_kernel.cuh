@@ -71,6 +71,18 @@ struct WarpLanes {
 #endif
         return x;
     }
+    // two independent butterfly sums interleaved (ILP)
+    __host__ __device__ static void sum2(double& a, double& b) {
+#ifdef __CUDA_ARCH__
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double x = __shfl_xor_sync(0xffffffffu, a, o);
+            const double y = __shfl_xor_sync(0xffffffffu, b, o);
+            a += x;
+            b += y;
+        }
+#endif
+    }
     __host__ __device__ static void sync() {
 #ifdef __CUDA_ARCH__
         __syncwarp();
@@ -83,6 +95,26 @@ struct WarpLanes {
         return *p;
 #endif
     }
+    // asynchronous global -> shared copy of n (even) doubles, 16 bytes per lane-chunk,
+    // L2 only (.cg): the ring is rewritten by CTA 0, so L1 must not serve stale lines
+    __host__ __device__ static void prefetch(double* dst, const double* src, int n) {
+#ifdef __CUDA_ARCH__
+        for (int c = (int)(threadIdx.x & 31); c < n / 2; c += 32) {
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + 2 * c);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src + 2 * c)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+#else
+        for (int j = 0; j < n; ++j) dst[j] = src[j];
+#endif
+    }
+    __host__ __device__ static void prefetch_wait() {
+#ifdef __CUDA_ARCH__
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncwarp();
+#endif
+    }
 };
 
 // --------------------------------------------------------------------------------------
@@ -91,6 +123,7 @@ struct KParams {
     int kind, d, ld, dd, rw, pw;
     int G, gP;                 // grid; SVM: CTAs [0, gP) hold P rows
     int tile_rows, stages, resident;   // rows per warp tile, stages per warp ring
+    int fold_mode;                     // kFoldTwoBarriers / kFoldRedundant / kFoldLast
     int64_t n, n1;
     const double* X;           // n x ld (ld even, padded with zeros)
     const double* radii;       // SES: n rounded up to even (zero padded)
@@ -109,6 +142,7 @@ struct KParams {
     double* y_tilde;
     double* best_y;
     int* status;
+    long long* timing;         // optional: per-phase clock64 sums of CTA 0 / thread 0
     uint32_t stage_stride;     // bytes per ring stage
     uint32_t rad_off;          // byte offset of the radii inside a stage
 };
@@ -163,14 +197,15 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 
 // grid barrier among the consumer warps of all CTAs (co-residency guaranteed by the
 // cooperative launch); `target` = (barrier ordinal) * G.
+// The CTA's writes are ordered before thread 0's release by bar.sync (release is
+// cumulative); the other threads' reads are ordered after its acquire by the second
+// bar.sync.  No full fences: one L2 reduction plus the acquire polling.
 __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
     consumer_sync();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1ull);
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
         while (ld_acquire(bar) < target) {
         }
-        __threadfence();
     }
     consumer_sync();
 }
@@ -262,6 +297,8 @@ struct SmemMap {
     uint64_t* empty;   // [kNW * SW]
     double* vec;       // 10 control vectors of dd8
     double* ytd;       // y_tilde dummy for CTAs != 0
+    double* evict;     // prefetched window entry (dd8)
+    double* pend;      // pending pd_counter state (dd8 + IterState)
     double* red;       // rw
     double* wpart;     // kNW x pw
     PassParams* pp;
@@ -275,7 +312,8 @@ __host__ __device__ inline int dd8_of(int dd) { return (dd + 1) & ~1; }
 __host__ __device__ inline size_t smem_fixed_bytes(int dd, int rw, int pw, int nstages) {
     size_t b = 0;
     b += 2 * (size_t)nstages * 8;                      // mbarriers
-    b += 11 * (size_t)dd8_of(dd) * 8;                  // control vectors + y_tilde dummy
+    b += 12 * (size_t)dd8_of(dd) * 8;                  // control vectors, y_tilde dummy, evict
+    b += ((size_t)dd8_of(dd) + sizeof(IterState) / 8) * 8;   // pending state
     b += (size_t)((rw + 1) & ~1) * 8;                  // red
     b += (size_t)kNW * ((pw + 1) & ~1) * 8;            // warp partials
     b += sizeof(PassParams) + sizeof(sc_ftp_result) + 16 * 4 + 64;
@@ -295,6 +333,10 @@ __device__ inline SmemMap carve(unsigned char* base, const KParams& p) {
     off += 10 * (size_t)dd8 * 8;
     m.ytd = reinterpret_cast<double*>(base + off);
     off += (size_t)dd8 * 8;
+    m.evict = reinterpret_cast<double*>(base + off);
+    off += (size_t)dd8 * 8;
+    m.pend = reinterpret_cast<double*>(base + off);
+    off += ((size_t)dd8 + sizeof(IterState) / 8) * 8;
     m.red = reinterpret_cast<double*>(base + off);
     off += (size_t)((p.rw + 1) & ~1) * 8;
     m.wpart = reinterpret_cast<double*>(base + off);
@@ -673,6 +715,42 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
 }
 
 // --------------------------------------------------------------------------------------
+// fold of all G CTA partials by one CTA: warp per FC-column chunk, lanes stride over the
+// partials, then a butterfly per column (fixed order: bitwise reproducible)
+enum FoldMode { kFoldTwoBarriers = 0, kFoldRedundant = 1, kFoldLast = 2 };
+
+template <int KIND>
+__device__ __forceinline__ void fold_all(const KParams& p, const SmemMap& m, bool publish) {
+    constexpr int FC = 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j0 = warp * FC; j0 < p.rw; j0 += kNW * FC) {
+        double acc[FC];
+        int op[FC];
+#pragma unroll
+        for (int k = 0; k < FC; ++k) {
+            op[k] = red_op(KIND, min(j0 + k, p.rw - 1));
+            acc[k] = op_identity(op[k]);
+        }
+        for (int q = lane; q < p.G; q += 32) {
+            const double* row = p.partials + (size_t)q * p.rw;
+#pragma unroll
+            for (int k = 0; k < FC; ++k)
+                if (j0 + k < p.rw) acc[k] = op_apply(op[k], acc[k], __ldcg(row + j0 + k));
+        }
+#pragma unroll
+        for (int k = 0; k < FC; ++k) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                acc[k] = op_apply(op[k], acc[k], __shfl_xor_sync(0xffffffffu, acc[k], o));
+            if (lane == 0 && j0 + k < p.rw) {
+                m.red[j0 + k] = acc[k];
+                if (publish) p.redg[j0 + k] = acc[k];
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------------------------------------
 // the persistent kernel
 template <int KIND, int LPR, int CPL, int NB>
 __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
@@ -707,7 +785,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
         ctl.v = CtlVecs{V, V + dd8, V + 2 * dd8, V + 3 * dd8, V + 4 * dd8, V + 5 * dd8,
                         V + 6 * dd8, V + 7 * dd8, V + 8 * dd8, V + 9 * dd8};
         const int sl = p.slot_len;
-        ctl.s = CtlSlots{p.ring, p.ring_cap, p.slots, p.slots + sl, p.slots + 2 * sl,
+        ctl.evict_buf = m.evict;
+        ctl.pend_buf = m.pend;
+        ctl.s = CtlSlots{p.ring, p.ring_cap, dd8, p.slots, p.slots + sl, p.slots + 2 * sl,
                          p.slots + 4 * sl};
         for (int j = lane; j < dd8; j += 32) {
             for (int q = 0; q < 10; ++q) V[q * dd8 + j] = 0.0;
@@ -724,6 +804,15 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
     // columns of the reduced vector folded by this CTA
     const int c0 = (int)((int64_t)b * p.rw / p.G), c1 = (int)((int64_t)(b + 1) * p.rw / p.G);
     const int pws = (p.pw + 1) & ~1;
+    const bool timed = p.timing != nullptr && b == 0 && tid == 0;
+    long long tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    long long tprev = timed ? clock64() : 0;
+#define SCMWU_TMARK(i)                               \
+    if (timed) {                                     \
+        const long long tnow = clock64();            \
+        tacc[i] += tnow - tprev;                     \
+        tprev = tnow;                                \
+    }
     while (pp->action == kPass) {
         const PassParams ps = *pp;
         if (KIND == SC_SES) {
@@ -733,7 +822,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
             if (ps.check) svm_pass<LPR, CPL, NB, true>(p, m, ps, r0, r1, ws, pass_idx, isP);
             else svm_pass<LPR, CPL, NB, false>(p, m, ps, r0, r1, ws, pass_idx, isP);
         }
+        SCMWU_TMARK(0)
         consumer_sync();
+        SCMWU_TMARK(1)
         // CTA partial, fixed warp order, written in the reduced layout
         const int nw_act = nwt < kNW ? nwt : kNW;   // warps that own at least one tile
         for (int j = tid; j < p.rw; j += kNW * 32) {
@@ -758,28 +849,80 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
             }
             p.partials[(size_t)b * p.rw + j] = v;
         }
-        grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
-        // column-distributed fold over the G partials: warp per column, fixed tree
-        for (int j = c0 + warp; j < c1; j += kNW) {
-            const int op = red_op(KIND, j);
-            double acc = op_identity(op);
-            for (int q = lane; q < p.G; q += 32)
-                acc = op_apply(op, acc, __ldcg(p.partials + (size_t)q * p.rw + j));
+        SCMWU_TMARK(2)
+        if (p.fold_mode == kFoldLast) {
+            // one global synchronisation: the CTA whose arrival completes the pass
+            // folds all partials (fixed tree) and publishes them with a release epoch
+            consumer_sync();
+            if (tid == 0) {
+                unsigned long long old;
+                asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                             : "=l"(old) : "l"(p.bar) : "memory");
+                m.flags[0] = old + 1 == (unsigned long long)(pass_idx + 1) * p.G ? 1 : 0;
+            }
+            consumer_sync();
+            SCMWU_TMARK(3)
+            if (m.flags[0]) {
+                fold_all<KIND>(p, m, true);
+                SCMWU_TMARK(4)
+                consumer_sync();
+                if (tid == 0)
+                    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.bar + 1),
+                                 "l"((unsigned long long)(pass_idx + 1))
+                                 : "memory");
+                SCMWU_TMARK(5)
+            } else {
+                SCMWU_TMARK(4)
+                if (tid == 0)
+                    while (ld_acquire(p.bar + 1) < (unsigned long long)(pass_idx + 1)) {
+                    }
+                consumer_sync();
+                SCMWU_TMARK(5)
+                for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
+            }
+            consumer_sync();
+            SCMWU_TMARK(6)
+        } else if (p.fold_mode == kFoldRedundant) {
+            // every CTA folds all G partials itself with the same fixed tree
+            grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
+            SCMWU_TMARK(3)
+            fold_all<KIND>(p, m, false);
+            SCMWU_TMARK(4)
+            consumer_sync();
+            SCMWU_TMARK(6)
+        } else {
+            grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
+            SCMWU_TMARK(3)
+            // column-distributed fold over the G partials: warp per column, fixed tree
+            for (int j = c0 + warp; j < c1; j += kNW) {
+                const int op = red_op(KIND, j);
+                double acc = op_identity(op);
+                for (int q = lane; q < p.G; q += 32)
+                    acc = op_apply(op, acc, __ldcg(p.partials + (size_t)q * p.rw + j));
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-                acc = op_apply(op, acc, __shfl_xor_sync(0xffffffffu, acc, o));
-            if (lane == 0) p.redg[j] = acc;
+                for (int o = 16; o > 0; o >>= 1)
+                    acc = op_apply(op, acc, __shfl_xor_sync(0xffffffffu, acc, o));
+                if (lane == 0) p.redg[j] = acc;
+            }
+            SCMWU_TMARK(4)
+            grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
+            SCMWU_TMARK(5)
+            for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
+            consumer_sync();
+            SCMWU_TMARK(6)
         }
-        grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
-        for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
-        consumer_sync();
         if (warp == 0) {
             int act = ctl.after_pass(m.red, p.red0, y_tilde, pp);
             if (lane == 0) pp->action = act;
         }
+        SCMWU_TMARK(7)
         consumer_sync();
+        SCMWU_TMARK(8)
         ++pass_idx;
     }
+#undef SCMWU_TMARK
+    if (timed)
+        for (int i = 0; i < 9; ++i) p.timing[i] = tacc[i];
     // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
     stream_drain(p, m, warp, ws);
     if (b == 0 && warp == 0) {

@@ -23,8 +23,13 @@ struct HostLanes {
     static int lane() { return 0; }
     static int nl() { return 1; }
     static double sum(double x) { return x; }
+    static void sum2(double&, double&) {}
     static void sync() {}
     static double ldcg(const double* p) { return *p; }
+    static void prefetch(double* dst, const double* src, int n) {
+        for (int j = 0; j < n; ++j) dst[j] = src[j];
+    }
+    static void prefetch_wait() {}
 };
 
 constexpr double kInvSqrt2 = 0.7071067811865476;
@@ -198,7 +203,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     c.res = res; c.writer = true;
     c.v = CtlVecs{ysum.data(), yprev.data(), wsum.data(), besty.data(), claimy.data(),
                   ywin.data(), zv.data(), ynew.data(), pU.data(), v1.data()};
-    c.s = CtlSlots{h->ring.data(), cap, h->pd_pending.data(), h->pd_callmin.data(),
+    c.s = CtlSlots{h->ring.data(), cap, dd, h->pd_pending.data(), h->pd_callmin.data(),
                    h->pd_sep.data(), h->last.data()};
     PassParams pp{};
     std::vector<double> red(red_width(h->prob.kind, d));
@@ -304,6 +309,11 @@ int sc_elapsed(sc_handle* h, float* ms) {
     return SC_OK;
 }
 int64_t sc_launches(const sc_handle* h) { (void)h; return 0; }
+int sc_debug_timing(sc_handle* h, double* out) {
+    if (!h || !out) return SC_EARG;
+    for (int i = 0; i < 9; ++i) out[i] = 0.0;
+    return SC_OK;
+}
 
 const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "null handle"; }
 

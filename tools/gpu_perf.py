@@ -47,6 +47,14 @@ def main():
         print(f"refine h={a.horizon}: {type(r).__name__} iters {r.iterations} passes {r.passes} "
               f"kernel {r.kernel_ms:.1f} ms -> {us:.2f} us/pass, "
               f"{bytes_pass / us / 1e3:.1f} GB/s", flush=True)
+        if os.environ.get("SCMWU_TIMING"):
+            t = dev.handle.debug_timing() / max(r.passes, 1)
+            names = ["pass", "join", "cta_part", "bar1", "fold", "bar2", "red_read", "tail",
+                     "tail_join"]
+            tot = t.sum()
+            print("  cycles/pass (CTA0 thread0): " + ", ".join(
+                f"{n}={v:.0f}" for n, v in zip(names, t)) + f"  total={tot:.0f} "
+                f"(~{tot / 1.9e3:.2f} us at 1.9 GHz)", flush=True)
     if a.full:
         dev.close()
         t0 = time.time()
