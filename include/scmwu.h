@@ -70,6 +70,14 @@ typedef struct {
     double ln_r;       /* math.log(rank) evaluated on the host (bit-exact with Python) */
     int32_t grid;      /* CTAs of the persistent kernel (0 = auto) */
     int32_t device;    /* CUDA device ordinal */
+    /* row sharding across GPUs (one process per GPU); world <= 1: single GPU.
+     * Rows [row0, row0 + n_local) of the global matrix live on this rank; n1_local of
+     * them (the first ones) are SVM P rows.  `n`, `n1`, D, rho, rank stay global. */
+    int32_t world;
+    int32_t shard;     /* this rank's index in [0, world) */
+    int64_t row0;
+    int64_t n_local;
+    int64_t n1_local;
 } sc_problem;
 
 /* One feasibility test. */
@@ -135,6 +143,24 @@ int64_t sc_launches(const sc_handle* h);
  * fold, barrier 2, reduced read, control tail, tail join); zeros otherwise. */
 int sc_debug_timing(sc_handle* h, double* out);
 int sc_pd_pair(sc_handle* h, double* mu /* n1 */, double* gam /* n - n1 */, double* dist);
+/* Row sharding (world > 1).  The per-pass exchange runs INSIDE the persistent kernel:
+ * each rank writes its folded pass vector into every peer's mailbox over NVLink and
+ * raises a system-scope flag; every rank folds the rank vectors in rank order.
+ *   sc_local_red0   this shard's contribution to the iterate-1 sums (red_width doubles)
+ *   sc_set_globals  the rank-ordered fold of those, plus the anchor row (SES v1, g1)
+ *   sc_ipc_handle   64-byte CUDA IPC handle of this rank's mailbox
+ *   sc_connect      map the world x 64-byte handles of all ranks (own included)
+ * For world <= 1 none of these is needed. */
+int sc_local_red0(sc_handle* h, double* out);
+/* progress extremes over this shard's rows: SES {max_i |v_i - y| + g_i, 0},
+ * SVM {min_P P.y, max_Q Q.y}; the caller folds ranks (max / min / max). */
+int sc_progress_parts(sc_handle* h, const double* y, double* out2);
+int sc_set_globals(sc_handle* h, const double* red0, const double* v1, double g1);
+int sc_ipc_handle(sc_handle* h, void* out64);
+int sc_connect(sc_handle* h, const void* handles);
+/* Local (this shard's) materialisation for sharded handles: sc_iterate writes the local
+ * block of p (SES: (n_local - [shard holds row 0]) blocks, SVM: n_local coordinates) and
+ * sc_pd_pair the unnormalised local weights; the host folds the shards. */
 int sc_set_grid(sc_handle* h, int32_t grid);
 int sc_info(const sc_handle* h, int64_t* out /* 8 values: grid, threads, lanes_per_row,
               cols_per_lane, tile_rows, stages, resident, smem_bytes */);

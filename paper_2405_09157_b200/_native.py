@@ -39,7 +39,9 @@ class ScProblem(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("d", ctypes.c_int32), ("n", ctypes.c_int64),
                 ("n1", ctypes.c_int64), ("D", ctypes.c_double), ("rho", ctypes.c_double),
                 ("R", ctypes.c_double), ("rank", ctypes.c_int64), ("ln_r", ctypes.c_double),
-                ("grid", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("grid", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("shard", ctypes.c_int32), ("row0", ctypes.c_int64),
+                ("n_local", ctypes.c_int64), ("n1_local", ctypes.c_int64)]
 
 
 class ScFtpArgs(ctypes.Structure):
@@ -66,7 +68,8 @@ class ScFtpResult(ctypes.Structure):
 
 EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "sc_pd_pair",
            "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_debug_timing",
-           "sc_last_error", "sc_destroy", "sc_version")
+           "sc_local_red0", "sc_progress_parts", "sc_set_globals", "sc_ipc_handle",
+           "sc_connect", "sc_last_error", "sc_destroy", "sc_version")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -107,17 +110,30 @@ class Engine:
         lib.sc_launches.argtypes = [vp]
         lib.sc_launches.restype = ctypes.c_int64
         lib.sc_debug_timing.argtypes = [vp, _dp]
+        lib.sc_local_red0.argtypes = [vp, _dp]
+        lib.sc_progress_parts.argtypes = [vp, _dp, _dp]
+        lib.sc_set_globals.argtypes = [vp, _dp, _dp, ctypes.c_double]
+        lib.sc_ipc_handle.argtypes = [vp, ctypes.c_char_p]
+        lib.sc_connect.argtypes = [vp, ctypes.c_char_p]
         self.lib = lib
 
     def create(self, kind: int, X, X_tail, radii, D: float, rho: float, R: float,
-               rank: int, n1: int = 0, grid: int = 0, device: int = 0) -> "Handle":
+               rank: int, n1: int = 0, grid: int = 0, device: int = 0,
+               shard: Optional[tuple] = None) -> "Handle":
+        """``shard = (world, index, row0, n_global)``: X holds rows [row0, row0 + len(X))
+        of an n_global-row matrix (one GPU of a row-sharded solve)."""
         X = np.ascontiguousarray(X, dtype=np.float64)
         Xt = None if X_tail is None else np.ascontiguousarray(X_tail, dtype=np.float64)
         rad = None if radii is None else np.ascontiguousarray(radii, dtype=np.float64)
         n = X.shape[0] + (0 if Xt is None else Xt.shape[0])
         d = X.shape[1]
+        world, index, row0, n_local = 1, 0, 0, n
+        if shard is not None and shard[0] > 1:
+            world, index, row0, n = shard
+        n1_local = max(0, min(n_local, n1 - row0)) if kind == SC_SVM else 0
         prob = ScProblem(kind=kind, d=d, n=n, n1=n1, D=D, rho=rho, R=R, rank=rank,
-                         ln_r=math.log(rank), grid=grid, device=device)
+                         ln_r=math.log(rank), grid=grid, device=device, world=world,
+                         shard=index, row0=row0, n_local=n_local, n1_local=n1_local)
         h = ctypes.c_void_p()
         st = self.lib.sc_create(ctypes.byref(prob), _ptr(X), _ptr(Xt), _ptr(rad),
                                 ctypes.byref(h))
@@ -187,8 +203,10 @@ class Handle:
         return float(f.value)
 
     def iterate(self) -> np.ndarray:
-        n, d = self.prob.n, self.prob.d
-        size = (n - 1) * (d + 1) if self.prob.kind == SC_SES else n
+        """p of the last call over this handle's rows (sharded: the local block)."""
+        n, d = self.prob.n_local, self.prob.d
+        first = 1 if self.prob.kind == SC_SES and self.prob.row0 == 0 else 0
+        size = (n - first) * (d + 1) if self.prob.kind == SC_SES else n
         out = np.empty(size)
         self._check(self.engine.lib.sc_iterate(self.h, _ptr(out)), "sc_iterate")
         return out
@@ -197,13 +215,44 @@ class Handle:
         self._check(self.engine.lib.sc_pd_commit(self.h, which), "sc_pd_commit")
 
     def pd_pair(self):
-        n1 = self.prob.n1
+        """(mu, gam, dist) for this handle's rows; sharded handles return the raw
+        local weights (dist NaN) and the caller normalises across ranks."""
+        n1 = self.prob.n1_local
         mu = np.empty(n1)
-        gam = np.empty(self.prob.n - n1)
+        gam = np.empty(self.prob.n_local - n1)
         dist = ctypes.c_double()
         self._check(self.engine.lib.sc_pd_pair(self.h, _ptr(mu), _ptr(gam), ctypes.byref(dist)),
                     "sc_pd_pair")
         return mu, gam, float(dist.value)
+
+    # ---- row sharding
+    def local_red0(self) -> np.ndarray:
+        rw = self.prob.d + (7 if self.prob.kind == SC_SES else 12 + self.prob.d)
+        out = np.zeros(rw)
+        self._check(self.engine.lib.sc_local_red0(self.h, _ptr(out)), "sc_local_red0")
+        return out
+
+    def set_globals(self, red0, v1=None, g1: float = 0.0) -> None:
+        red0 = np.ascontiguousarray(red0, dtype=np.float64)
+        v = None if v1 is None else np.ascontiguousarray(v1, dtype=np.float64)
+        self._check(self.engine.lib.sc_set_globals(self.h, _ptr(red0), _ptr(v), g1),
+                    "sc_set_globals")
+
+    def progress_parts(self, y) -> np.ndarray:
+        y = np.ascontiguousarray(np.asarray(y, dtype=np.float64)[: self.d])
+        out = np.zeros(2)
+        self._check(self.engine.lib.sc_progress_parts(self.h, _ptr(y), _ptr(out)),
+                    "sc_progress_parts")
+        return out
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        self._check(self.engine.lib.sc_ipc_handle(self.h, buf), "sc_ipc_handle")
+        return buf.raw
+
+    def connect(self, handles: list) -> None:
+        blob = b"".join(handles)
+        self._check(self.engine.lib.sc_connect(self.h, blob), "sc_connect")
 
     def pd_reset(self) -> None:
         self._check(self.engine.lib.sc_pd_commit(self.h, 2), "sc_pd_commit")

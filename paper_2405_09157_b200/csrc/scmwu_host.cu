@@ -44,12 +44,12 @@ __global__ void progress_kernel(const double* X, const double* radii, int64_t n,
 // iterate materialisation: p for SES blocks / SVM coordinates, from an IterState slot.
 __global__ void iterate_kernel(const double* X, const double* radii, int64_t n, int64_t n1,
                                int d, int ld, int kind, const double* slot, int dd, double rho,
-                               double alpha, double* out) {
+                               double alpha, double* out, int64_t first) {
     const IterState st = *reinterpret_cast<const IterState*>(slot + dd + (dd & 1));
     const double er = st.eta / rho;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (kind == SC_SES) {
-        if (i < 1 || i >= n) return;
+        if (i < first || i >= n) return;   // local rows; global row 0 is the anchor
         const double* v = X + i * ld;
         const double g = radii[i];
         double a = 0.0;
@@ -60,7 +60,7 @@ __global__ void iterate_kernel(const double* X, const double* radii, int64_t n, 
         const double A = exp((x0 + nrm) * kInvSqrt2 - st.shift);
         const double B = exp((x0 - nrm) * kInvSqrt2 - st.shift);
         const double cc = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
-        double* o = out + (i - 1) * (d + 1);
+        double* o = out + (i - first) * (d + 1);
         for (int j = 0; j < d; ++j) {
             const double x = fma(-st.t, v[j], slot[j]);
             o[j] = (cc * (-er * x)) / st.T;
@@ -152,6 +152,12 @@ struct sc_handle {
     double *y_tilde = nullptr, *best_y = nullptr, *scratch = nullptr, *yvec = nullptr;
     int* status = nullptr;
     long long* timing = nullptr;     // SCMWU_TIMING=1: per-phase cycle sums of the last call
+    double* v1 = nullptr;            // SES anchor row
+    // sharding: this rank's mailbox (flags + 2 x world x rw doubles) and the peers'
+    void* mbox_base = nullptr;
+    void* peer_base[kMaxWorld] = {};
+    bool connected = false;
+    int64_t pass_total = 0;          // passes of all previous calls (identical on all ranks)
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, mk0 = nullptr, mk1 = nullptr;
     int64_t launches = 0;
@@ -174,23 +180,24 @@ static int cuda_fail(sc_handle* h, cudaError_t e, const char* what) {
 static int configure(sc_handle* h, int grid_req) {
     const int d = h->prob.d;
     const int RPW = 32 / h->cfg.lpr;
-    const int64_t n = h->prob.n;
+    const int64_t n = h->prob.n_local;
     // grid: one CTA per SM, at most one CTA per warp-step of rows
     int G = grid_req > 0 ? grid_req : h->sms;
     const int64_t step = (int64_t)kNW * RPW;
     if (grid_req <= 0) G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + step - 1) / step));
-    if (h->prob.kind == SC_SVM) G = std::max(G, 2);
+    const int64_t n1 = h->prob.kind == SC_SVM ? h->prob.n1_local : 0, n2 = n - n1;
+    const bool two_sided = h->prob.kind == SC_SVM && n1 > 0 && n2 > 0;
+    if (two_sided) G = std::max(G, 2);
     G = std::min(G, h->sms);
     if (G < 1) G = 1;
-    if (h->prob.kind == SC_SVM && G < 2) { h->err = "SVM needs >= 2 SMs"; return SC_EARG; }
-    // rows -> CTAs
+    if (two_sided && G < 2) { h->err = "SVM needs >= 2 SMs"; return SC_EARG; }
+    // rows -> CTAs (SVM: P-CTAs then Q-CTAs, each CTA single-sided)
     std::vector<int64_t> rb(G + 1);
-    if (h->prob.kind == SC_SES) {
+    if (h->prob.kind == SC_SES || !two_sided) {
         for (int b = 0; b <= G; ++b) rb[b] = (int64_t)((__int128)n * b / G) & ~(int64_t)1;
         rb[G] = n;
-        h->gP = 0;
+        h->gP = h->prob.kind == SC_SVM && n1 > 0 ? G : 0;   // one-sided SVM shard
     } else {
-        const int64_t n1 = h->prob.n1, n2 = n - n1;
         int gP = (int)llround((double)G * (double)n1 / (double)n);
         gP = std::max(1, std::min(G - 1, gP));
         for (int b = 0; b <= gP; ++b) rb[b] = (int64_t)((__int128)n1 * b / gP);
@@ -252,8 +259,23 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail, con
     sc_handle* h = new sc_handle();
     *out = h;
     h->prob = *prob;
+    // row sharding: normalise the single-GPU case, validate the shard
+    sc_problem& P = h->prob;
+    if (P.world <= 1) {
+        P.world = 1; P.shard = 0; P.row0 = 0; P.n_local = P.n;
+        P.n1_local = P.kind == SC_SVM ? P.n1 : 0;
+    } else {
+        if (P.world > kMaxWorld || P.shard < 0 || P.shard >= P.world || P.n_local < 1 ||
+            P.row0 < 0 || P.row0 + P.n_local > P.n || X_tail) {
+            h->err = "bad row shard";
+            return SC_EARG;
+        }
+        P.n1_local = P.kind == SC_SVM
+                         ? std::max<int64_t>(0, std::min<int64_t>(P.n_local, P.n1 - P.row0))
+                         : 0;
+    }
     const int d = prob->d;
-    const int64_t n = prob->n;
+    const int64_t n = P.n_local;   // rows resident on this GPU
     if (!pick_cfg(d, h->cfg)) { h->err = "d > 512 is not supported yet"; return SC_EARG; }
     h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl, h->cfg.nb);
     if (!h->fn) { h->err = "no kernel instantiated for this d"; return SC_EARG; }
@@ -298,22 +320,29 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail, con
         CK(cudaMalloc(&h->radii, (size_t)(nr + 2) * 8), "alloc radii");
         CK(cudaMemset(h->radii, 0, (size_t)(nr + 2) * 8), "zero radii");
         CK(cudaMemcpy(h->radii, radii, (size_t)n * 8, cudaMemcpyHostToDevice), "copy radii");
-        h->g1 = radii[0];
+        h->g1 = P.row0 == 0 ? radii[0] : 0.0;   // sharded: sc_set_globals provides it
     }
-    // reduced vector of iterate 1 (cum = 0: every exponent 0)
+    // SES anchor row (global row 0; sharded: sc_set_globals provides it)
+    CK(cudaMalloc(&h->v1, (size_t)d * 8), "alloc anchor");
+    CK(cudaMemset(h->v1, 0, (size_t)d * 8), "zero anchor");
+    if (P.row0 == 0) CK(cudaMemcpy(h->v1, X, (size_t)d * 8, cudaMemcpyHostToDevice), "anchor");
+    // reduced vector of iterate 1 (cum = 0: every exponent 0) over the LOCAL rows;
+    // sharded handles get the rank-ordered fold through sc_set_globals
     h->red0_h.assign(h->rw, 0.0);
     if (prob->kind == SC_SES) {
         double rad = 0.0;
-        for (int64_t i = 1; i < n; ++i) rad += 2.0 * radii[i];
-        h->red0_h[kS_T] = 2.0 * (double)(n - 1);
+        const int64_t first = P.row0 == 0 ? 1 : 0;   // global row 0 is not a block
+        for (int64_t i = first; i < n; ++i) rad += 2.0 * radii[i];
+        h->red0_h[kS_T] = 2.0 * (double)(n - first);
         h->red0_h[kS_Rad] = rad;
     } else {
-        h->red0_h[kV_TP] = (double)prob->n1;
-        h->red0_h[kV_TQ] = (double)(n - prob->n1);
+        const int64_t n1l = P.n1_local;
+        h->red0_h[kV_TP] = (double)n1l;
+        h->red0_h[kV_TQ] = (double)(n - n1l);
         double* cs = nullptr;
         CK(cudaMalloc(&cs, 2 * (size_t)d * 8), "alloc colsum");
-        colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, 0, prob->n1, d, h->ld, cs);
-        colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, prob->n1, n, d, h->ld, cs + d);
+        colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, 0, n1l, d, h->ld, cs);
+        colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, n1l, n, d, h->ld, cs + d);
         CK(cudaStreamSynchronize(h->stream), "colsum");
         CK(cudaMemcpy(h->red0_h.data() + kV_Vec, cs, 2 * (size_t)d * 8, cudaMemcpyDeviceToHost),
            "copy colsum");
@@ -387,6 +416,18 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     p.status = h->status; p.stage_stride = h->stage_stride; p.rad_off = h->rad_off;
     if (!h->timing && getenv("SCMWU_TIMING")) CK(cudaMalloc(&h->timing, 16 * 8), "alloc timing");
     p.timing = h->timing;
+    p.v1 = h->v1;
+    p.world = h->prob.world;
+    p.shard = h->prob.shard;
+    p.row0 = h->prob.row0;
+    p.pass_base = h->pass_total;
+    if (p.world > 1) {
+        if (!h->connected) { h->err = "sharded handle is not connected (sc_connect)"; return SC_EARG; }
+        for (int r = 0; r < p.world; ++r) {
+            p.mflag[r] = reinterpret_cast<unsigned long long*>(h->peer_base[r]);
+            p.mbox[r] = reinterpret_cast<double*>(static_cast<char*>(h->peer_base[r]) + 64 * 8);
+        }
+    }
     CK(cudaMemsetAsync(h->bar, 0, 64, h->stream), "reset barrier");
     CK(cudaMemsetAsync(h->res, 0, sizeof(sc_ftp_result), h->stream), "reset result");
     CK(cudaMemsetAsync(h->status, 0xff, sizeof(int), h->stream), "reset status");
@@ -406,6 +447,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h->ev0, h->ev1);
     res->kernel_ms = ms;
+    h->pass_total += res->passes;
     h->has_callmin = res->has_counter_min != 0;
     h->has_sep = res->kind == SC_PRIMAL;
     if (status == SC_EWIDTH) { h->err = "width violation"; return SC_EWIDTH; }
@@ -413,14 +455,15 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     return SC_OK;
 }
 
-int sc_progress(sc_handle* h, const double* y, double* f) {
-    if (!h || !y || !f) return SC_EARG;
+int sc_progress_parts(sc_handle* h, const double* y, double* out) {
+    if (!h || !y || !out) return SC_EARG;
     CK(cudaSetDevice(h->prob.device), "set device");
     const int d = h->prob.d;
     CK(cudaMemcpyAsync(h->yvec, y, d * 8, cudaMemcpyHostToDevice, h->stream), "copy y");
     const int blocks = std::min(h->sms * 4, 2048);
-    progress_kernel<<<blocks, 256, 0, h->stream>>>(h->X, h->radii, h->prob.n, h->prob.n1, d,
-                                                   h->ld, h->prob.kind, h->yvec, h->scratch);
+    progress_kernel<<<blocks, 256, 0, h->stream>>>(h->X, h->radii, h->prob.n_local,
+                                                   h->prob.n1_local, d, h->ld, h->prob.kind,
+                                                   h->yvec, h->scratch);
     h->launches += 1;
     CK(cudaGetLastError(), "progress kernel");
     std::vector<double> part(2 * blocks);
@@ -430,28 +473,96 @@ int sc_progress(sc_handle* h, const double* y, double* f) {
     if (h->prob.kind == SC_SES) {
         double m = -INFINITY;
         for (int b = 0; b < blocks; ++b) m = std::max(m, part[2 * b]);
-        *f = m;
+        out[0] = m;
+        out[1] = 0.0;
     } else {
-        double mp = INFINITY, mq = -INFINITY, nrm = 0.0;
-        for (int b = 0; b < blocks; ++b) { mp = std::min(mp, part[2 * b]); mq = std::max(mq, part[2 * b + 1]); }
-        for (int j = 0; j < d; ++j) nrm += y[j] * y[j];
-        nrm = sqrt(nrm);
-        *f = Control<WarpLanes>::svm_margin(mp, mq, nrm);
+        double mp = INFINITY, mq = -INFINITY;
+        for (int b = 0; b < blocks; ++b) {
+            mp = std::min(mp, part[2 * b]);
+            mq = std::max(mq, part[2 * b + 1]);
+        }
+        out[0] = mp;
+        out[1] = mq;
     }
+    return SC_OK;
+}
+
+int sc_progress(sc_handle* h, const double* y, double* f) {
+    if (!h || !y || !f) return SC_EARG;
+    if (h->prob.world > 1) { h->err = "sharded handle: use sc_progress_parts"; return SC_EARG; }
+    double parts[2];
+    int st = sc_progress_parts(h, y, parts);
+    if (st != SC_OK) return st;
+    if (h->prob.kind == SC_SES) {
+        *f = parts[0];
+    } else {
+        double nrm = 0.0;
+        for (int j = 0; j < h->prob.d; ++j) nrm += y[j] * y[j];
+        *f = Control<WarpLanes>::svm_margin(parts[0], parts[1], sqrt(nrm));
+    }
+    return SC_OK;
+}
+
+int sc_local_red0(sc_handle* h, double* out) {
+    if (!h || !out) return SC_EARG;
+    for (int j = 0; j < h->rw; ++j) out[j] = h->red0_h[j];
+    return SC_OK;
+}
+
+int sc_set_globals(sc_handle* h, const double* red0, const double* v1, double g1) {
+    if (!h || !red0) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    for (int j = 0; j < h->rw; ++j) h->red0_h[j] = red0[j];
+    CK(cudaMemcpy(h->red0, red0, h->rw * 8, cudaMemcpyHostToDevice), "copy red0");
+    if (v1) CK(cudaMemcpy(h->v1, v1, h->prob.d * 8, cudaMemcpyHostToDevice), "copy anchor");
+    h->g1 = g1;
+    return SC_OK;
+}
+
+static size_t mbox_bytes(const sc_handle* h) {
+    return 64 * 8 + 2 * (size_t)h->prob.world * h->rw * 8;
+}
+
+int sc_ipc_handle(sc_handle* h, void* out64) {
+    if (!h || !out64 || h->prob.world <= 1) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    if (!h->mbox_base) {
+        CK(cudaMalloc(&h->mbox_base, mbox_bytes(h)), "alloc mailbox");
+        CK(cudaMemset(h->mbox_base, 0, mbox_bytes(h)), "zero mailbox");
+    }
+    cudaIpcMemHandle_t ih;
+    CK(cudaIpcGetMemHandle(&ih, h->mbox_base), "ipc handle");
+    static_assert(sizeof(ih) == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(out64, &ih, 64);
+    return SC_OK;
+}
+
+int sc_connect(sc_handle* h, const void* handles) {
+    if (!h || !handles || h->prob.world <= 1 || !h->mbox_base) return SC_EARG;
+    CK(cudaSetDevice(h->prob.device), "set device");
+    for (int r = 0; r < h->prob.world; ++r) {
+        if (r == h->prob.shard) { h->peer_base[r] = h->mbox_base; continue; }
+        cudaIpcMemHandle_t ih;
+        memcpy(&ih, static_cast<const char*>(handles) + 64 * r, 64);
+        CK(cudaIpcOpenMemHandle(&h->peer_base[r], ih, cudaIpcMemLazyEnablePeerAccess),
+           "open peer mailbox");
+    }
+    h->connected = true;
     return SC_OK;
 }
 
 int sc_iterate(sc_handle* h, double* out) {
     if (!h || !out) return SC_EARG;
     CK(cudaSetDevice(h->prob.device), "set device");
-    const int64_t n = h->prob.n;
-    const int64_t size = h->prob.kind == SC_SES ? (n - 1) * (h->prob.d + 1) : n;
+    const int64_t n = h->prob.n_local;
+    const int64_t first = h->prob.kind == SC_SES && h->prob.row0 == 0 ? 1 : 0;
+    const int64_t size = h->prob.kind == SC_SES ? (n - first) * (h->prob.d + 1) : n;
     double* buf = nullptr;
-    CK(cudaMalloc(&buf, (size_t)size * 8), "alloc iterate");
+    CK(cudaMalloc(&buf, (size_t)std::max<int64_t>(size, 1) * 8), "alloc iterate");
     // the `last` slot holds the latest iterate's state (written by the last sc_ftp)
     iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
-        h->X, h->radii, n, h->prob.n1, h->prob.d, h->ld, h->prob.kind,
-        h->slots + 4 * h->slot_len, h->dd, h->prob.rho, h->last_alpha, buf);
+        h->X, h->radii, n, h->prob.n1_local, h->prob.d, h->ld, h->prob.kind,
+        h->slots + 4 * h->slot_len, h->dd, h->prob.rho, h->last_alpha, buf, first);
     h->launches += 1;
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e == cudaSuccess) e = cudaMemcpy(out, buf, (size_t)size * 8, cudaMemcpyDeviceToHost);
@@ -477,7 +588,7 @@ int sc_pd_commit(sc_handle* h, int32_t which) {
 int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
     if (!h || h->prob.kind != SC_SVM || !mu || !gam || !dist) return SC_EARG;
     CK(cudaSetDevice(h->prob.device), "set device");
-    const int64_t n = h->prob.n, n1 = h->prob.n1;
+    const int64_t n = h->prob.n_local, n1 = h->prob.n1_local;
     const int d = h->prob.d;
     double* buf = nullptr;
     CK(cudaMalloc(&buf, (size_t)n * 8), "alloc pair");
@@ -493,22 +604,29 @@ int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
     }
     iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
         h->X, h->radii, n, n1, d, h->ld, SC_SVM, h->slots + 3 * h->slot_len, h->dd, h->prob.rho,
-        0.0, buf);
+        0.0, buf, 0);
     h->launches += 1;
     std::vector<double> e(n);
     cudaError_t ce = cudaStreamSynchronize(h->stream);
     if (ce == cudaSuccess) ce = cudaMemcpy(e.data(), buf, (size_t)n * 8, cudaMemcpyDeviceToHost);
     cudaFree(buf);
     if (ce != cudaSuccess) return cuda_fail(h, ce, "pd pair");
+    if (h->prob.world > 1) {   // sharded: raw local weights, the host normalises globally
+        for (int64_t i = 0; i < n1; ++i) mu[i] = e[i];
+        for (int64_t i = n1; i < n; ++i) gam[i - n1] = e[i];
+        *dist = NAN;
+        return SC_OK;
+    }
     double sP = 0.0, sQ = 0.0;
     for (int64_t i = 0; i < n1; ++i) sP += e[i];
     for (int64_t i = n1; i < n; ++i) sQ += e[i];
     for (int64_t i = 0; i < n1; ++i) mu[i] = e[i] / sP;
     for (int64_t i = n1; i < n; ++i) gam[i - n1] = e[i] / sQ;
     // distance of the uniform pair from the column sums; callers keep the committed one
+    const int64_t N1 = h->prob.n1, N = h->prob.n;
     double s = 0.0;
     for (int j = 0; j < d; ++j) {
-        double z = h->red0_h[kV_Vec + j] / (double)n1 - h->red0_h[kV_Vec + d + j] / (double)(n - n1);
+        double z = h->red0_h[kV_Vec + j] / (double)N1 - h->red0_h[kV_Vec + d + j] / (double)(N - N1);
         s += z * z;
     }
     *dist = sqrt(s);
@@ -555,7 +673,9 @@ void sc_destroy(sc_handle* h) {
     cudaSetDevice(h->prob.device);
     void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar, h->timing,
                     h->ring, h->slots, h->res, h->y_tilde, h->best_y, h->scratch, h->yvec,
-                    h->status};
+                    h->status, h->v1, h->mbox_base};
+    for (int r = 0; r < kMaxWorld; ++r)
+        if (h->peer_base[r] && h->peer_base[r] != h->mbox_base) cudaIpcCloseMemHandle(h->peer_base[r]);
     for (void* b : bufs)
         if (b) cudaFree(b);
     if (h->ev0) cudaEventDestroy(h->ev0);

@@ -48,6 +48,7 @@ constexpr int kThreads = kNW * 32;          // 256 threads: up to 255 registers
 constexpr int kNumSlots = 5;                // pending, callmin, sep, best, last
 constexpr double kInvSqrt2 = 0.7071067811865476;
 constexpr int kMaxSmem = 232448;            // 227 KB opt-in per CTA on sm_100
+constexpr int kMaxWorld = 8;                // GPUs of one NVLink/NVSwitch node
 
 struct WarpLanes {
     __host__ __device__ static int lane() {
@@ -143,6 +144,13 @@ struct KParams {
     double* best_y;
     int* status;
     long long* timing;         // optional: per-phase clock64 sums of CTA 0 / thread 0
+    const double* v1;          // SES anchor row (d values)
+    // row sharding across GPUs (world > 1): mailboxes in every rank's HBM, mapped here
+    int world, shard;
+    int64_t row0;              // global index of this rank's first row
+    int64_t pass_base;         // passes run by earlier calls (mailbox parity / flag epochs)
+    double* mbox[kMaxWorld];   // rank r's mailbox data [2][world][rw] (peer pointers)
+    unsigned long long* mflag[kMaxWorld];   // rank r's arrival flags [world]
     uint32_t stage_stride;     // bytes per ring stage
     uint32_t rad_off;          // byte offset of the radii inside a stage
 };
@@ -537,7 +545,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                 F = fmax(F, fma(ra, inv_t, g));
                 if (CHECK) Fw = fmax(Fw, sqrt(v[NV - 1][0]) + g);
             }
-            if (a + r > 0) {
+            if (p.row0 + a + r > 0) {   // global row 0 is the anchor, not a block
                 const double nrm = er * ra;
                 const double x0 = -er_t * (al - g);
                 const double lp = (x0 + nrm) * kInvSqrt2, lm = (x0 - nrm) * kInvSqrt2;
@@ -763,6 +771,8 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
     const bool isP = KIND == SC_SVM && b < p.gP;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNW * p.stages; ++s) mbar_init(&m.full[s], 1);
+        m.flags[0] = 0;
+        m.flags[1] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -791,7 +801,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
                          p.slots + 4 * sl};
         for (int j = lane; j < dd8; j += 32) {
             for (int q = 0; q < 10; ++q) V[q * dd8 + j] = 0.0;
-            if (KIND == SC_SES && j < p.d) V[9 * dd8 + j] = p.X[j];   // anchor v1
+            if (KIND == SC_SES && j < p.d) V[9 * dd8 + j] = p.v1[j];   // anchor v1
         }
         __syncwarp();
         int act = ctl.begin(p.args, p.red0, y_tilde, nullptr, pp);
@@ -902,14 +912,63 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1)
                     acc = op_apply(op, acc, __shfl_xor_sync(0xffffffffu, acc, o));
-                if (lane == 0) p.redg[j] = acc;
+                if (lane == 0) {
+                    if (p.world > 1) {
+                        // this rank's folded column -> slot [parity][shard] of EVERY
+                        // rank's mailbox (NVLink stores to the peers' HBM)
+                        const size_t off =
+                            ((size_t)((p.pass_base + pass_idx) & 1) * p.world + p.shard) * p.rw + j;
+                        for (int r = 0; r < p.world; ++r) p.mbox[r][off] = acc;
+                        __threadfence_system();
+                    } else {
+                        p.redg[j] = acc;
+                    }
+                }
             }
             SCMWU_TMARK(4)
             grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
             SCMWU_TMARK(5)
-            for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
+            if (p.world > 1) {
+                // all of this rank's columns are out: raise our flag on every rank, then
+                // wait for every rank's flag and fold the rank vectors in rank order
+                // flags are monotone pass counters across calls: no reset race between ranks
+                const unsigned long long want = (unsigned long long)(p.pass_base + pass_idx + 1);
+                if (tid == 0 && b == 0)
+                    for (int r = 0; r < p.world; ++r)
+                        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[r] +
+                                                                                 p.shard),
+                                     "l"(want)
+                                     : "memory");
+                if (tid == 0) {
+                    const long long t0 = clock64();
+                    for (int r = 0; r < p.world; ++r) {
+                        unsigned long long v;
+                        do {
+                            asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+                                         : "=l"(v) : "l"(p.mflag[p.shard] + r) : "memory");
+                            if (clock64() - t0 > (1ll << 37)) { m.flags[1] = 1; break; }
+                        } while (v < want);
+                    }
+                }
+                consumer_sync();
+                const double* mb =
+                    p.mbox[p.shard] + (size_t)((p.pass_base + pass_idx) & 1) * p.world * p.rw;
+                for (int j = tid; j < p.rw; j += kNW * 32) {
+                    const int op = red_op(KIND, j);
+                    double acc = op_identity(op);
+                    for (int r = 0; r < p.world; ++r)
+                        acc = op_apply(op, acc, __ldcg(mb + (size_t)r * p.rw + j));
+                    m.red[j] = acc;
+                }
+            } else {
+                for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
+            }
             consumer_sync();
             SCMWU_TMARK(6)
+        }
+        if (m.flags[1]) {   // a peer never arrived: give up with an exchange error
+            if (b == 0 && tid == 0) *p.status = SC_ENCCL;
+            break;
         }
         if (warp == 0) {
             int act = ctl.after_pass(m.red, p.red0, y_tilde, pp);
@@ -928,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
     if (b == 0 && warp == 0) {
         for (int j = lane; j < p.dd; j += 32) p.best_y[j] = ctl.v.besty[j];
         if (lane == 0) {
-            *p.status = ctl.status;
+            if (!m.flags[1]) *p.status = ctl.status;
             p.res->passes = pass_idx;
         }
     }

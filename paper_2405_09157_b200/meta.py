@@ -110,6 +110,10 @@ class DeviceProblem:
             self.best_pd_dist = out.counter_min
         return out
 
+    def pd_pair(self):
+        """(mu^, gam^, dist) of the best committed pd_counter state (SVM)."""
+        return self.handle.pd_pair()
+
     def offer_separation(self, dist: float) -> None:
         """pd_counter(cert.p) side effect at a separation (R/svm.py:201-204)."""
         if self.best_pd_dist is None or dist < self.best_pd_dist:

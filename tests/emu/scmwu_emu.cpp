@@ -5,11 +5,18 @@
 // loop that computes the streaming pass row by row with the same closed-form
 // formulas as the CUDA kernel.  It exports the sc_* C ABI of include/scmwu.h
 // so the host layer can be exercised on a machine without a GPU
-// (tests/test_emu_*.py).  It is never loaded by the product package.
+// (tests/test_emu_*.py, tests/test_multirank_gloo.py).  It is never loaded by
+// the product package.
+//
+// Row sharding: where the CUDA kernel exchanges the per-pass rank vectors over
+// NVLink mailboxes, the emulator calls a host callback (emu_set_exchange) that
+// the multi-process CPU tests implement with a torch.distributed (gloo)
+// all-gather followed by the same rank-ordered fold.
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -36,12 +43,18 @@ constexpr double kInvSqrt2 = 0.7071067811865476;
 
 }  // namespace
 
+typedef void (*emu_exchange_fn)(const double* local, int rw, double* global);
+
 struct sc_handle {
     sc_problem prob;
     int dd;
-    std::vector<double> X, radii;       // n x d, n
-    std::vector<double> red0;
+    std::vector<double> X, radii;       // n_local x d, n_local
+    std::vector<double> red0, red0_local;
+    std::vector<double> v1;
+    double g1 = 0.0;
+    double last_alpha = 0.0;
     std::vector<double> ring, pd_pending, pd_callmin, pd_sep, pd_best, last;
+    emu_exchange_fn exchange = nullptr;
     std::string err;
 };
 
@@ -55,7 +68,7 @@ static int slot_len(int dd) { return dd + (dd & 1) + (int)(sizeof(IterState) / s
 static void pass_ses(const sc_handle* h, const PassParams& pp, const double* U,
                      const double* up, const double* yw, double* red) {
     const int d = h->prob.d;
-    const int64_t n = h->prob.n;
+    const int64_t n = h->prob.n_local;
     double T = 0, Lin = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
     std::vector<double> Sd(d, 0.0), df(d);
     const double t = pp.t, er = pp.eta_rho, al = pp.alpha;
@@ -75,7 +88,7 @@ static void pass_ses(const sc_handle* h, const PassParams& pp, const double* U,
         const double ra = sqrt(a);
         F = fmax(F, ra / t + g);
         if (pp.check) Fw = fmax(Fw, sqrt(f2) + g);
-        if (i == 0) continue;
+        if (h->prob.row0 + i == 0) continue;   // global row 0 is the anchor
         const double nrm = er * ra;
         const double x0 = -er * (t * (al - g));
         const double lp = (x0 + nrm) * kInvSqrt2, lm = (x0 - nrm) * kInvSqrt2;
@@ -96,7 +109,7 @@ static void pass_ses(const sc_handle* h, const PassParams& pp, const double* U,
 static void pass_svm(const sc_handle* h, const PassParams& pp, const double* W,
                      const double* wp, const double* yw, const double* z, double* red) {
     const int d = h->prob.d;
-    const int64_t n = h->prob.n, n1 = h->prob.n1;
+    const int64_t n = h->prob.n_local, n1 = h->prob.n1_local;
     double TP = 0, TQ = 0, M = -INFINITY, mrP = INFINITY, mrQ = INFINITY, Wd = 0;
     double mPW = INFINITY, xQW = -INFINITY, mPy = INFINITY, xQy = -INFINITY;
     double mPz = INFINITY, xQz = -INFINITY;
@@ -136,6 +149,10 @@ extern "C" {
 
 int sc_version(void) { return 1000; }
 
+void emu_set_exchange(sc_handle* h, emu_exchange_fn fn) {
+    if (h) h->exchange = fn;
+}
+
 int sc_create(const sc_problem* prob, const double* X, const double* X_tail,
               const double* radii, sc_handle** out) {
     if (!prob || !X || !out) return SC_EARG;
@@ -144,8 +161,22 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail,
     if (prob->kind == SC_SVM && (prob->n1 < 1 || prob->n1 >= prob->n)) return SC_EARG;
     sc_handle* h = new sc_handle();
     h->prob = *prob;
+    sc_problem& P = h->prob;
+    if (P.world <= 1) {
+        P.world = 1; P.shard = 0; P.row0 = 0; P.n_local = P.n;
+        P.n1_local = P.kind == SC_SVM ? P.n1 : 0;
+    } else {
+        if (P.shard < 0 || P.shard >= P.world || P.n_local < 1 || P.row0 < 0 ||
+            P.row0 + P.n_local > P.n || X_tail) {
+            delete h;
+            return SC_EARG;
+        }
+        P.n1_local = P.kind == SC_SVM
+                         ? std::max<int64_t>(0, std::min<int64_t>(P.n_local, P.n1 - P.row0))
+                         : 0;
+    }
     const int d = prob->d;
-    const int64_t n = prob->n;
+    const int64_t n = P.n_local;
     h->dd = prob->kind == SC_SES ? d + 1 : d + 2;
     if (X_tail) {
         h->X.assign(X, X + prob->n1 * d);
@@ -154,20 +185,28 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail,
         h->X.assign(X, X + n * d);
     }
     if (prob->kind == SC_SES) h->radii.assign(radii, radii + n);
+    h->v1.assign(h->dd, 0.0);
+    if (P.row0 == 0 && prob->kind == SC_SES) {
+        for (int j = 0; j < d; ++j) h->v1[j] = h->X[j];
+        h->g1 = h->radii[0];
+    }
     h->red0.assign(red_width(prob->kind, d), 0.0);
     if (prob->kind == SC_SES) {
+        const int64_t first = P.row0 == 0 ? 1 : 0;
         double rad = 0;
-        for (int64_t i = 1; i < n; ++i) rad += 2.0 * h->radii[i];
-        h->red0[kS_T] = 2.0 * (double)(n - 1);
+        for (int64_t i = first; i < n; ++i) rad += 2.0 * h->radii[i];
+        h->red0[kS_T] = 2.0 * (double)(n - first);
         h->red0[kS_Rad] = rad;
         h->red0[kS_M] = 0.0;
     } else {
-        h->red0[kV_TP] = (double)prob->n1;
-        h->red0[kV_TQ] = (double)(n - prob->n1);
+        const int64_t n1 = P.n1_local;
+        h->red0[kV_TP] = (double)n1;
+        h->red0[kV_TQ] = (double)(n - n1);
         for (int64_t i = 0; i < n; ++i)
             for (int j = 0; j < d; ++j)
-                h->red0[kV_Vec + (i < prob->n1 ? 0 : d) + j] += h->X[i * d + j];
+                h->red0[kV_Vec + (i < n1 ? 0 : d) + j] += h->X[i * d + j];
     }
+    h->red0_local = h->red0;
     const int sl = slot_len(h->dd);
     h->pd_pending.assign(sl, 0.0);
     h->pd_callmin.assign(sl, 0.0);
@@ -184,36 +223,40 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     memset(res, 0, sizeof(*res));
     const int d = h->prob.d, dd = h->dd;
     const int64_t T = args->mode == SC_MODE_FTP ? args->budget : args->horizon;
-    if (T < 1) return fail(h, SC_EARG, "budget/horizon must be >= 1");
+    if (T < 0 || (args->mode == SC_MODE_REFINE && T < 1))
+        return fail(h, SC_EARG, "budget/horizon out of range");
+    if (h->prob.world > 1 && !h->exchange) return fail(h, SC_EARG, "no exchange callback");
+    h->last_alpha = args->alpha;
     // the ring holds at most max(64, T_rung/2)+1 live entries; the largest rung is <= T
     int64_t cap = (T / 2 > kLadderBase ? T / 2 : kLadderBase) + 2;
     if (args->mode == SC_MODE_FTP && cap > (1 << 24)) cap = (1 << 24);
     h->ring.assign((size_t)cap * dd, 0.0);
 
     std::vector<double> ysum(dd), yprev(dd), wsum(dd), besty(dd), claimy(dd), ywin(dd),
-        zv(dd), ynew(dd), pU(dd), v1(dd, 0.0);
-    if (h->prob.kind == SC_SES)
-        for (int j = 0; j < d; ++j) v1[j] = h->X[j];
+        zv(dd), ynew(dd), pU(dd), v1(h->v1);
     Control<HostLanes> c;
     c.kind = h->prob.kind; c.d = d; c.dd = dd;
     c.is_max = h->prob.kind == SC_SES;
     c.rho = h->prob.rho; c.inv_rho = 1.0 / h->prob.rho; c.R = h->prob.R;
     c.ln_r = h->prob.ln_r; c.D = h->prob.D;
-    c.g1 = h->prob.kind == SC_SES ? h->radii[0] : 0.0;
+    c.g1 = h->g1;
     c.res = res; c.writer = true;
     c.v = CtlVecs{ysum.data(), yprev.data(), wsum.data(), besty.data(), claimy.data(),
                   ywin.data(), zv.data(), ynew.data(), pU.data(), v1.data()};
     c.s = CtlSlots{h->ring.data(), cap, dd, h->pd_pending.data(), h->pd_callmin.data(),
                    h->pd_sep.data(), h->last.data()};
     PassParams pp{};
-    std::vector<double> red(red_width(h->prob.kind, d));
+    const int rw = red_width(h->prob.kind, d);
+    std::vector<double> red(rw), loc(rw);
     int act = c.begin(*args, h->red0.data(), y_tilde, best_y, &pp);
     int64_t passes = 0;
     while (act == kPass) {
+        double* dst = h->prob.world > 1 ? loc.data() : red.data();
         if (h->prob.kind == SC_SES)
-            pass_ses(h, pp, ysum.data(), yprev.data(), ywin.data(), red.data());
+            pass_ses(h, pp, ysum.data(), yprev.data(), ywin.data(), dst);
         else
-            pass_svm(h, pp, ysum.data(), yprev.data(), ywin.data(), zv.data(), red.data());
+            pass_svm(h, pp, ysum.data(), yprev.data(), ywin.data(), zv.data(), dst);
+        if (h->prob.world > 1) h->exchange(loc.data(), rw, red.data());
         ++passes;
         act = c.after_pass(red.data(), h->red0.data(), y_tilde, &pp);
     }
@@ -223,10 +266,10 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     return c.status;
 }
 
-int sc_progress(sc_handle* h, const double* y, double* f) {
-    if (!h || !y || !f) return SC_EARG;
+int sc_progress_parts(sc_handle* h, const double* y, double* out) {
+    if (!h || !y || !out) return SC_EARG;
     const int d = h->prob.d;
-    const int64_t n = h->prob.n;
+    const int64_t n = h->prob.n_local;
     if (h->prob.kind == SC_SES) {
         double best = -INFINITY;
         for (int64_t i = 0; i < n; ++i) {
@@ -234,20 +277,51 @@ int sc_progress(sc_handle* h, const double* y, double* f) {
             for (int j = 0; j < d; ++j) { double x = h->X[i * d + j] - y[j]; s = fma(x, x, s); }
             best = fmax(best, sqrt(s) + h->radii[i]);
         }
-        *f = best;
+        out[0] = best;
+        out[1] = 0.0;
     } else {
-        double nrm = 0, mP = INFINITY, xQ = -INFINITY;
-        for (int j = 0; j < d; ++j) nrm += y[j] * y[j];
-        nrm = sqrt(nrm);
+        double mP = INFINITY, xQ = -INFINITY;
         for (int64_t i = 0; i < n; ++i) {
             double s = 0;
             for (int j = 0; j < d; ++j) s = fma(h->X[i * d + j], y[j], s);
-            if (i < h->prob.n1) mP = fmin(mP, s); else xQ = fmax(xQ, s);
+            if (i < h->prob.n1_local) mP = fmin(mP, s); else xQ = fmax(xQ, s);
         }
-        *f = Control<HostLanes>::svm_margin(mP, xQ, nrm);
+        out[0] = mP;
+        out[1] = xQ;
     }
     return SC_OK;
 }
+
+int sc_progress(sc_handle* h, const double* y, double* f) {
+    if (!h || !y || !f || h->prob.world > 1) return SC_EARG;
+    double parts[2];
+    sc_progress_parts(h, y, parts);
+    if (h->prob.kind == SC_SES) {
+        *f = parts[0];
+    } else {
+        double nrm = 0;
+        for (int j = 0; j < h->prob.d; ++j) nrm += y[j] * y[j];
+        *f = Control<HostLanes>::svm_margin(parts[0], parts[1], sqrt(nrm));
+    }
+    return SC_OK;
+}
+
+int sc_local_red0(sc_handle* h, double* out) {
+    if (!h || !out) return SC_EARG;
+    std::copy(h->red0_local.begin(), h->red0_local.end(), out);
+    return SC_OK;
+}
+
+int sc_set_globals(sc_handle* h, const double* red0, const double* v1, double g1) {
+    if (!h || !red0) return SC_EARG;
+    std::copy(red0, red0 + h->red0.size(), h->red0.begin());
+    if (v1) std::copy(v1, v1 + h->prob.d, h->v1.begin());
+    h->g1 = g1;
+    return SC_OK;
+}
+
+int sc_ipc_handle(sc_handle* h, void* out64) { (void)h; (void)out64; return SC_EARG; }
+int sc_connect(sc_handle* h, const void* handles) { (void)h; (void)handles; return SC_EARG; }
 
 int sc_pd_commit(sc_handle* h, int32_t which) {
     if (!h || h->prob.kind != SC_SVM) return SC_EARG;
@@ -261,7 +335,7 @@ int sc_pd_commit(sc_handle* h, int32_t which) {
 int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
     if (!h || h->prob.kind != SC_SVM || !mu || !gam || !dist) return SC_EARG;
     const int d = h->prob.d, dd = h->dd;
-    const int64_t n = h->prob.n, n1 = h->prob.n1;
+    const int64_t n = h->prob.n_local, n1 = h->prob.n1_local;
     const double* W = h->pd_best.data();
     const IterState st = *reinterpret_cast<const IterState*>(W + dd + (dd & 1));
     const double er = st.eta / h->prob.rho;
@@ -274,6 +348,11 @@ int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
         double lg = -er * ((P ? 1.0 : -1.0) * dW - (P ? W[d] : W[d + 1]));
         e[i] = exp(lg - st.shift);
         (P ? sP : sQ) += e[i];
+    }
+    if (h->prob.world > 1) {
+        for (int64_t i = 0; i < n; ++i) (i < n1 ? mu[i] : gam[i - n1]) = e[i];
+        *dist = NAN;
+        return SC_OK;
     }
     std::vector<double> z(d, 0.0);
     for (int64_t i = 0; i < n; ++i) {

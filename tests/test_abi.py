@@ -18,7 +18,7 @@ HEADER = os.path.join(ROOT, "include", "scmwu.h")
 
 def _declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(sc_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sc_[a-z_0-9]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
