@@ -48,7 +48,7 @@ WORKLOADS = {
 }
 # GPU iteration counts of full solves measured by this bench (profiles/); used only by the
 # reference arm to extrapolate the CPU port's s/iter to a time-to-eps.
-ITERS_EST = {"ses_c2": 15_515, "svm_c3": 300_000, "ses_c1": 82_518, "ses_c4": 360_000}
+ITERS_EST = {"ses_c2": 15_515, "svm_c3": 320_146, "ses_c1": 103_672, "ses_c4": 360_000}
 
 
 def make_instance(w):
