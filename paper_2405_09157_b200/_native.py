@@ -302,5 +302,6 @@ def cuda_engine() -> Engine:
     """The B200 engine (paper_2405_09157_b200/libscmwu.so).  Raises if absent."""
     global _cuda_engine
     if _cuda_engine is None:
-        _cuda_engine = Engine(os.path.join(PKG_DIR, LIB_NAME))
+        # SCMWU_LIB: an alternative build of the same CUDA engine (A/B performance runs)
+        _cuda_engine = Engine(os.environ.get("SCMWU_LIB") or os.path.join(PKG_DIR, LIB_NAME))
     return _cuda_engine

@@ -32,6 +32,11 @@
 #else
 #define SC_HD inline
 #endif
+#if defined(__CUDA_ARCH__) && defined(SCMWU_TAIL_UNROLL)
+#define SC_UNROLL4 _Pragma("unroll 4")
+#else
+#define SC_UNROLL4
+#endif
 
 namespace scmwu {
 
@@ -170,7 +175,7 @@ struct Control {
         if (!better(f)) return;
         has_best_f = true; best_f = f;
         const double inv_t = 1.0 / (double)t;
-#pragma unroll 4
+SC_UNROLL4
         for (int j = L::lane(); j < dd; j += L::nl()) v.besty[j] = v.ysum[j] * inv_t;
     }
     SC_HD void offer_vec(double f, const double* y) {
@@ -335,7 +340,7 @@ struct Control {
             const double coef = -(eta * inv_rho) / Tt;
             // one reduction for |s|^2 and s.v1: s.u = s.v1 + (alpha - g1) |s|^2 / |s|
             double s2 = 0.0, sv = 0.0;
-#pragma unroll 4
+SC_UNROLL4
             for (int j = ln; j < d; j += nl) {
                 const double sj = coef * red[kS_Vec + j];
                 v.ynew[j] = sj;          // temporarily s
@@ -346,7 +351,7 @@ struct Control {
             const double sn = sqrt(s2);
             const double am = a.alpha - g1;
             const double inv_sn = sn > 0.0 ? 1.0 / sn : 0.0;
-#pragma unroll 4
+SC_UNROLL4
             for (int j = ln; j < d; j += nl) v.ynew[j] = fma(am * inv_sn, v.ynew[j], v.v1[j]);
             const double su = sn > 0.0 ? fma(am * inv_sn, s2, sv) : sv;
             const double lin = coef * red[kS_Lin];
@@ -363,7 +368,7 @@ struct Control {
             cur.S1 = v.ysum[d]; cur.S2 = v.ysum[d + 1];
             const double inv_T = 1.0 / Tt;
             double g2 = 0.0;
-#pragma unroll 4
+SC_UNROLL4
             for (int j = ln; j < d; j += nl) {
                 const double gj = (red[kV_Vec + j] - red[kV_Vec + d + j]) * inv_T;
                 v.ynew[j] = gj;
@@ -372,7 +377,7 @@ struct Control {
             g2 = L::sum(g2);
             const double gn = sqrt(g2);
             const double inv_gn = gn > 0.0 ? 1.0 / gn : 0.0;
-#pragma unroll 4
+SC_UNROLL4
             for (int j = ln; j < d; j += nl)
                 v.ynew[j] = gn > 0.0 ? v.ynew[j] * inv_gn : (j == 0 ? 1.0 : 0.0);
             const double gw = gn > 0.0 ? g2 * inv_gn : 0.0;       // g . w
@@ -393,7 +398,7 @@ struct Control {
             // pd_counter at this iterate (R/svm.py:173-181): z = GP/TP - GQ/TQ
             const double iP = 1.0 / red[kV_TP], iQ = 1.0 / red[kV_TQ];
             double z2 = 0.0;
-#pragma unroll 4
+SC_UNROLL4
             for (int j = ln; j < d; j += nl) {
                 const double z = red[kV_Vec + j] * iP - red[kV_Vec + d + j] * iQ;
                 v.zv[j] = z;
@@ -405,7 +410,7 @@ struct Control {
             if (pend_buf != nullptr) keep_state(pend_buf, v.ysum, cur);
         }
         double* slot = s.ring + (win_count % s.ring_cap) * s.ring_stride;
-#pragma unroll 4
+SC_UNROLL4
         for (int j = ln; j < dd; j += nl) {
             const double y = v.ynew[j];
             v.pU[j] = v.ysum[j];
@@ -420,7 +425,7 @@ struct Control {
         push_window(k);
         if (chk) {
             const double inv_len = 1.0 / (double)win_len;
-#pragma unroll 4
+SC_UNROLL4
             for (int j = ln; j < dd; j += nl) v.ywin[j] = v.wsum[j] * inv_len;
         }
         // lagged shift for the next pass: the max eigenvalue / logit of this iterate

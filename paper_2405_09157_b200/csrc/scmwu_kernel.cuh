@@ -49,6 +49,13 @@ constexpr int kNumSlots = 5;                // pending, callmin, sep, best, last
 constexpr double kInvSqrt2 = 0.7071067811865476;
 constexpr int kMaxSmem = 232448;            // 227 KB opt-in per CTA on sm_100
 constexpr int kMaxWorld = 8;                // GPUs of one NVLink/NVSwitch node
+// build variants for A/B measurements (-DSCMWU_LEAN drops the experimental fold modes
+// and the multi-GPU exchange from the kernel body)
+#ifdef SCMWU_LEAN
+constexpr bool kFoldVariants = false, kMultiGpu = false;
+#else
+constexpr bool kFoldVariants = true, kMultiGpu = true;
+#endif
 
 struct WarpLanes {
     __host__ __device__ static int lane() {
@@ -727,8 +734,44 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
 // partials, then a butterfly per column (fixed order: bitwise reproducible)
 enum FoldMode { kFoldTwoBarriers = 0, kFoldRedundant = 1, kFoldLast = 2 };
 
+// Multi-GPU exchange (after this rank's columns went out to every mailbox and the
+// local grid barrier): raise our flag on every rank, wait for every rank's flag, fold
+// the rank vectors in rank order into `red`.  Flags are monotone pass counters across
+// calls (no reset race); a 2^37-cycle timeout reports a missing peer via flags[1].
+// Out of line: it must not cost the streaming loop registers.
 template <int KIND>
-__device__ __forceinline__ void fold_all(const KParams& p, const SmemMap& m, bool publish) {
+static __device__ __noinline__ void rank_exchange(const KParams& p, double* red,
+                                                  volatile int* flags, int pass_idx) {
+    const int tid = threadIdx.x;
+    const unsigned long long want = (unsigned long long)(p.pass_base + pass_idx + 1);
+    if (tid == 0 && blockIdx.x == 0)
+        for (int r = 0; r < p.world; ++r)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[r] + p.shard),
+                         "l"(want)
+                         : "memory");
+    if (tid == 0) {
+        const long long t0 = clock64();
+        for (int r = 0; r < p.world; ++r) {
+            unsigned long long v;
+            do {
+                asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+                             : "=l"(v) : "l"(p.mflag[p.shard] + r) : "memory");
+                if (clock64() - t0 > (1ll << 37)) { flags[1] = 1; break; }
+            } while (v < want);
+        }
+    }
+    consumer_sync();
+    const double* mb = p.mbox[p.shard] + (size_t)((p.pass_base + pass_idx) & 1) * p.world * p.rw;
+    for (int j = tid; j < p.rw; j += kNW * 32) {
+        const int op = red_op(KIND, j);
+        double acc = op_identity(op);
+        for (int r = 0; r < p.world; ++r) acc = op_apply(op, acc, __ldcg(mb + (size_t)r * p.rw + j));
+        red[j] = acc;
+    }
+}
+
+template <int KIND>
+static __device__ __noinline__ void fold_all(const KParams& p, double* red, bool publish) {
     constexpr int FC = 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j0 = warp * FC; j0 < p.rw; j0 += kNW * FC) {
@@ -751,7 +794,7 @@ __device__ __forceinline__ void fold_all(const KParams& p, const SmemMap& m, boo
             for (int o = 16; o > 0; o >>= 1)
                 acc[k] = op_apply(op[k], acc[k], __shfl_xor_sync(0xffffffffu, acc[k], o));
             if (lane == 0 && j0 + k < p.rw) {
-                m.red[j0 + k] = acc[k];
+                red[j0 + k] = acc[k];
                 if (publish) p.redg[j0 + k] = acc[k];
             }
         }
@@ -761,7 +804,7 @@ __device__ __forceinline__ void fold_all(const KParams& p, const SmemMap& m, boo
 // --------------------------------------------------------------------------------------
 // the persistent kernel
 template <int KIND, int LPR, int CPL, int NB>
-__global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
+__global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constant__ KParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SmemMap m = carve(smem, p);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -814,7 +857,13 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
     // columns of the reduced vector folded by this CTA
     const int c0 = (int)((int64_t)b * p.rw / p.G), c1 = (int)((int64_t)(b + 1) * p.rw / p.G);
     const int pws = (p.pw + 1) & ~1;
+    // per-phase timing only in -DSCMWU_PHASE_TIMING builds: the nine live counters
+    // would otherwise cost registers in the streaming loop of every build
+#ifdef SCMWU_PHASE_TIMING
     const bool timed = p.timing != nullptr && b == 0 && tid == 0;
+#else
+    constexpr bool timed = false;
+#endif
     long long tacc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long tprev = timed ? clock64() : 0;
 #define SCMWU_TMARK(i)                               \
@@ -860,7 +909,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
             p.partials[(size_t)b * p.rw + j] = v;
         }
         SCMWU_TMARK(2)
-        if (p.fold_mode == kFoldLast) {
+        if (kFoldVariants && p.fold_mode == kFoldLast) {
             // one global synchronisation: the CTA whose arrival completes the pass
             // folds all partials (fixed tree) and publishes them with a release epoch
             consumer_sync();
@@ -873,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
             consumer_sync();
             SCMWU_TMARK(3)
             if (m.flags[0]) {
-                fold_all<KIND>(p, m, true);
+                fold_all<KIND>(p, m.red, true);
                 SCMWU_TMARK(4)
                 consumer_sync();
                 if (tid == 0)
@@ -892,11 +941,11 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
             }
             consumer_sync();
             SCMWU_TMARK(6)
-        } else if (p.fold_mode == kFoldRedundant) {
+        } else if (kFoldVariants && p.fold_mode == kFoldRedundant) {
             // every CTA folds all G partials itself with the same fixed tree
             grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
             SCMWU_TMARK(3)
-            fold_all<KIND>(p, m, false);
+            fold_all<KIND>(p, m.red, false);
             SCMWU_TMARK(4)
             consumer_sync();
             SCMWU_TMARK(6)
@@ -913,7 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
                 for (int o = 16; o > 0; o >>= 1)
                     acc = op_apply(op, acc, __shfl_xor_sync(0xffffffffu, acc, o));
                 if (lane == 0) {
-                    if (p.world > 1) {
+                    if (kMultiGpu && p.world > 1) {
                         // this rank's folded column -> slot [parity][shard] of EVERY
                         // rank's mailbox (NVLink stores to the peers' HBM)
                         const size_t off =
@@ -928,38 +977,8 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const KParams p) {
             SCMWU_TMARK(4)
             grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
             SCMWU_TMARK(5)
-            if (p.world > 1) {
-                // all of this rank's columns are out: raise our flag on every rank, then
-                // wait for every rank's flag and fold the rank vectors in rank order
-                // flags are monotone pass counters across calls: no reset race between ranks
-                const unsigned long long want = (unsigned long long)(p.pass_base + pass_idx + 1);
-                if (tid == 0 && b == 0)
-                    for (int r = 0; r < p.world; ++r)
-                        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[r] +
-                                                                                 p.shard),
-                                     "l"(want)
-                                     : "memory");
-                if (tid == 0) {
-                    const long long t0 = clock64();
-                    for (int r = 0; r < p.world; ++r) {
-                        unsigned long long v;
-                        do {
-                            asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
-                                         : "=l"(v) : "l"(p.mflag[p.shard] + r) : "memory");
-                            if (clock64() - t0 > (1ll << 37)) { m.flags[1] = 1; break; }
-                        } while (v < want);
-                    }
-                }
-                consumer_sync();
-                const double* mb =
-                    p.mbox[p.shard] + (size_t)((p.pass_base + pass_idx) & 1) * p.world * p.rw;
-                for (int j = tid; j < p.rw; j += kNW * 32) {
-                    const int op = red_op(KIND, j);
-                    double acc = op_identity(op);
-                    for (int r = 0; r < p.world; ++r)
-                        acc = op_apply(op, acc, __ldcg(mb + (size_t)r * p.rw + j));
-                    m.red[j] = acc;
-                }
+            if (kMultiGpu && p.world > 1) {
+                rank_exchange<KIND>(p, m.red, m.flags, pass_idx);
             } else {
                 for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
             }
@@ -1000,6 +1019,6 @@ typedef void (*KernelFn)(const KParams);
 
 // explicit instantiation + lookup, used by the scmwu_inst_*.cu translation units
 #define SCMWU_INST(K, L, C, B)                                                          \
-    template __global__ void scmwu::scmwu_kernel<K, L, C, B>(const scmwu::KParams);
+    template __global__ void scmwu::scmwu_kernel<K, L, C, B>(const __grid_constant__ scmwu::KParams);
 #define SCMWU_MATCH(K, L, C, B) \
     if (kind == K && lpr == L && cpl == C && nb == B) return scmwu::scmwu_kernel<K, L, C, B>;

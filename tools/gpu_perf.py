@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--horizon", type=int, default=2048)
+    ap.add_argument("--ftp", action="store_true", help="solve_ftp (rung ladder) instead of refine")
+    ap.add_argument("--alpha", type=float, default=None)
     a = ap.parse_args()
     w = bench.WORKLOADS[a.workload]
     t0 = time.time()
@@ -41,8 +43,13 @@ def main():
     print(f"upload {time.time()-t0:.2f}s info {json.dumps(dev.handle.info())}", flush=True)
     st = meta.EarlyStopConfig(enabled=False)
     bytes_pass = bench.alg_bytes_per_pass(w)
+    if a.alpha is not None:
+        alpha = a.alpha
     for rep in range(3):
-        r = meta.refine_run(spec, alpha, a.horizon, st, dev.progress)
+        if a.ftp:
+            r = meta.solve_ftp(spec, alpha, 1e-9, st, dev.progress, a.horizon)
+        else:
+            r = meta.refine_run(spec, alpha, a.horizon, st, dev.progress)
         us = r.kernel_ms * 1e3 / max(r.passes, 1)
         print(f"refine h={a.horizon}: {type(r).__name__} iters {r.iterations} passes {r.passes} "
               f"kernel {r.kernel_ms:.1f} ms -> {us:.2f} us/pass, "
