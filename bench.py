@@ -51,11 +51,32 @@ WORKLOADS = {
 ITERS_EST = {"ses_c2": 15_515, "svm_c3": 320_146, "ses_c1": 103_672, "ses_c4": 360_000}
 
 
-def make_instance(w):
-    from paper_2405_09157_b200 import instances
+def make_instance(w, pinned=False):
+    """The workload's instance; ``pinned`` places the point arrays in page-locked host
+    memory (the e2e contract: inputs are copied to the device from pinned memory)."""
+    from paper_2405_09157_b200 import instances, ses, svm
     if w["kind"] == "ses":
-        return instances.gen_ses(w["n"], w["d"], w["seed"], w["dist"])
-    inst, _ = instances.gen_svm(w["n1"], w["n2"], w["d"], w["seed"], w["gap"])
+        inst = instances.gen_ses(w["n"], w["d"], w["seed"], w["dist"])
+    else:
+        inst, _ = instances.gen_svm(w["n1"], w["n2"], w["d"], w["seed"], w["gap"])
+    if not pinned:
+        return inst
+
+    def pin(a):
+        import torch
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+        out = t.numpy()          # shares the pinned buffer; `t` is kept alive below
+        out[...] = a
+        return out, t
+
+    if w["kind"] == "ses":
+        (c, tc), (r, tr) = pin(inst.centers), pin(inst.radii)
+        inst = ses.SesInstance(centers=c, radii=r)
+        make_instance._keep = (tc, tr)
+    else:
+        (P, tp), (Q, tq) = pin(inst.P), pin(inst.Q)
+        inst = svm.SvmInstance(P=P, Q=Q)
+        make_instance._keep = (tp, tq)
     return inst
 
 
@@ -207,7 +228,7 @@ def our_arm(args, w, rank, world):
         tdist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    inst = make_instance(w)
+    inst = make_instance(w, pinned=torch.cuda.is_available())
     t_up = time.perf_counter()
     comm = None
     if dist:

@@ -244,6 +244,48 @@ static int configure(sc_handle* h, int grid_req) {
     return SC_OK;
 }
 
+// Host rows (pitch d) -> device rows (pitch ld).  Pinned (page-locked / registered)
+// input is copied directly; pageable input goes through two pinned 32 MB staging
+// buffers so the host memcpy of one chunk overlaps the DMA of the other.
+static int upload_rows(sc_handle* h, double* dst, const double* src, int64_t rows, int d) {
+    if (rows <= 0) return SC_OK;
+    const size_t rowb = (size_t)d * 8, dpitch = (size_t)h->ld * 8;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, src) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+        CK(cudaMemcpy2DAsync(dst, dpitch, src, rowb, rowb, rows, cudaMemcpyHostToDevice,
+                             h->stream), "copy X (pinned)");
+        CK(cudaStreamSynchronize(h->stream), "copy X");
+        return SC_OK;
+    }
+    cudaGetLastError();   // clear the lookup error on pageable memory
+    const int64_t chunk = std::max<int64_t>(1, (int64_t)(32u << 20) / (int64_t)rowb);
+    void* stage[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+    int status = SC_OK;
+    for (int i = 0; i < 2 && status == SC_OK; ++i) {
+        if (cudaMallocHost(&stage[i], (size_t)chunk * rowb) != cudaSuccess ||
+            cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) != cudaSuccess)
+            status = SC_EOOM;
+    }
+    for (int64_t a = 0, k = 0; status == SC_OK && a < rows; a += chunk, ++k) {
+        const int64_t m = std::min(chunk, rows - a);
+        const int i = (int)(k & 1);
+        if (k >= 2 && cudaEventSynchronize(done[i]) != cudaSuccess) { status = SC_ECUDA; break; }
+        memcpy(stage[i], src + a * d, (size_t)m * rowb);
+        if (cudaMemcpy2DAsync(dst + a * h->ld, dpitch, stage[i], rowb, rowb, m,
+                              cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+            cudaEventRecord(done[i], h->stream) != cudaSuccess)
+            status = SC_ECUDA;
+    }
+    if (cudaStreamSynchronize(h->stream) != cudaSuccess && status == SC_OK) status = SC_ECUDA;
+    for (int i = 0; i < 2; ++i) {
+        if (stage[i]) cudaFreeHost(stage[i]);
+        if (done[i]) cudaEventDestroy(done[i]);
+    }
+    if (status != SC_OK) h->err = "staged upload of X failed";
+    return status;
+}
+
 extern "C" {
 
 int sc_version(void) { return 1000; }
@@ -302,19 +344,10 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail, con
     const size_t xbytes = (size_t)n * h->ld * sizeof(double);
     CK(cudaMalloc(&h->X, xbytes), "alloc X");
     const int64_t n_head = X_tail ? prob->n1 : n;
-    if (h->ld == d) {
-        CK(cudaMemcpy(h->X, X, (size_t)n_head * d * 8, cudaMemcpyHostToDevice), "copy X");
-        if (X_tail)
-            CK(cudaMemcpy(h->X + n_head * d, X_tail, (size_t)(n - n_head) * d * 8,
-                          cudaMemcpyHostToDevice), "copy X tail");
-    } else {
-        CK(cudaMemset(h->X, 0, xbytes), "zero X");
-        CK(cudaMemcpy2D(h->X, h->ld * 8, X, d * 8, d * 8, n_head, cudaMemcpyHostToDevice),
-           "copy X");
-        if (X_tail)
-            CK(cudaMemcpy2D(h->X + n_head * h->ld, h->ld * 8, X_tail, d * 8, d * 8, n - n_head,
-                            cudaMemcpyHostToDevice), "copy X tail");
-    }
+    if (h->ld != d) CK(cudaMemset(h->X, 0, xbytes), "zero X");
+    int up = upload_rows(h, h->X, X, n_head, d);
+    if (up == SC_OK && X_tail) up = upload_rows(h, h->X + n_head * h->ld, X_tail, n - n_head, d);
+    if (up != SC_OK) return up;
     if (prob->kind == SC_SES) {
         const int64_t nr = (n + 1) & ~(int64_t)1;
         CK(cudaMalloc(&h->radii, (size_t)(nr + 2) * 8), "alloc radii");
