@@ -112,22 +112,25 @@ static bool pick_cfg(int d, LaunchCfg& c) {
 
 // kernels are instantiated in scmwu_inst_*.cu (compiled in parallel)
 namespace scmwu {
-KernelFn scmwu_lookup_0(int kind, int lpr, int cpl, int nb);
-KernelFn scmwu_lookup_1(int kind, int lpr, int cpl, int nb);
-KernelFn scmwu_lookup_2(int kind, int lpr, int cpl, int nb);
-KernelFn scmwu_lookup_3(int kind, int lpr, int cpl, int nb);
-KernelFn scmwu_lookup_4(int kind, int lpr, int cpl, int nb);
-KernelFn scmwu_lookup_5(int kind, int lpr, int cpl, int nb);
-KernelFn scmwu_lookup_6(int kind, int lpr, int cpl, int nb);
-KernelFn scmwu_lookup_7(int kind, int lpr, int cpl, int nb);
+KernelFn scmwu_lookup_0(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_1(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_2(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_3(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_4(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_5(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_6(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_7(int kind, int lpr, int cpl, int nb, bool full);
 }  // namespace scmwu
 
-static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb) {
-    KernelFn (*fns[])(int, int, int, int) = {scmwu_lookup_0, scmwu_lookup_1, scmwu_lookup_2,
-                                        scmwu_lookup_3, scmwu_lookup_4, scmwu_lookup_5,
-                                        scmwu_lookup_6, scmwu_lookup_7};
+// full: every column slot but the last is in range (d > lpr * (cpl - 1)); instantiated
+// for SES only (measured: no gain for SVM)
+static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb, bool full) {
+    KernelFn (*fns[])(int, int, int, int, bool) = {scmwu_lookup_0, scmwu_lookup_1,
+                                                   scmwu_lookup_2, scmwu_lookup_3,
+                                                   scmwu_lookup_4, scmwu_lookup_5,
+                                                   scmwu_lookup_6, scmwu_lookup_7};
     for (auto f : fns)
-        if (KernelFn k = f(kind, lpr, cpl, nb)) return k;
+        if (KernelFn k = f(kind, lpr, cpl, nb, full)) return k;
     return nullptr;
 }
 
@@ -319,7 +322,8 @@ int sc_create(const sc_problem* prob, const double* X, const double* X_tail, con
     const int d = prob->d;
     const int64_t n = P.n_local;   // rows resident on this GPU
     if (!pick_cfg(d, h->cfg)) { h->err = "d > 512 is not supported yet"; return SC_EARG; }
-    h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl, h->cfg.nb);
+    const bool full = prob->kind == SC_SES && d > h->cfg.lpr * (h->cfg.cpl - 1);
+    h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl, h->cfg.nb, full);
     if (!h->fn) { h->err = "no kernel instantiated for this d"; return SC_EARG; }
     h->dd = prob->kind == SC_SES ? d + 1 : d + 2;
     h->ld = (d + 1) & ~1;

@@ -1,15 +1,19 @@
 // scmwu_inst_7.cu — explicit instantiations of the persistent kernel (part 7 of 8).
 #include "scmwu_kernel.cuh"
 
-SCMWU_INST(SC_SVM, 4, 4, 4)
-SCMWU_INST(SC_SVM, 8, 8, 4)
-SCMWU_INST(SC_SVM, 16, 12, 2)
+SCMWU_INST(SC_SES, 4, 3, 4, true)
+SCMWU_INST(SC_SES, 4, 8, 4, false)
+SCMWU_INST(SC_SVM, 8, 8, 4, false)
+SCMWU_INST(SC_SES, 8, 16, 2, true)
+SCMWU_INST(SC_SES, 32, 12, 2, false)
 
 namespace scmwu {
-KernelFn scmwu_lookup_7(int kind, int lpr, int cpl, int nb) {
-    SCMWU_MATCH(SC_SVM, 4, 4, 4)
-    SCMWU_MATCH(SC_SVM, 8, 8, 4)
-    SCMWU_MATCH(SC_SVM, 16, 12, 2)
+KernelFn scmwu_lookup_7(int kind, int lpr, int cpl, int nb, bool full) {
+    SCMWU_MATCH(SC_SES, 4, 3, 4, true)
+    SCMWU_MATCH(SC_SES, 4, 8, 4, false)
+    SCMWU_MATCH(SC_SVM, 8, 8, 4, false)
+    SCMWU_MATCH(SC_SES, 8, 16, 2, true)
+    SCMWU_MATCH(SC_SES, 32, 12, 2, false)
     return nullptr;
 }
 }  // namespace scmwu
