@@ -41,6 +41,8 @@ WORKLOADS = {
                    desc="SES n=10^6 d=100 uniform-in-ball points, eps=1e-3 (BASELINE configs[1])"),
     "svm_c3": dict(kind="svm", n1=500_000, n2=500_000, d=100, seed=0, gap=1.0, eps=1e-3,
                    desc="hard-margin SVM n=10^6 (5e5+5e5) d=100 gap 1, eps=1e-3 (configs[2])"),
+    "ses_d100_small": dict(kind="ses", n=4_000, d=100, dist="uniform-ball", seed=0, eps=1e-3,
+                           desc="SES n=4000 d=100 (shared-memory resident; diagnostics)"),
     "ses_c1": dict(kind="ses", n=10_000, d=10, dist="gaussian", seed=0, eps=1e-2,
                    desc="SES n=10^4 d=10 Gaussian, eps=1e-2 (configs[0])"),
     "ses_c4": dict(kind="ses", n=10 ** 7, d=100, dist="uniform-ball", seed=0, eps=1e-3,

@@ -138,9 +138,12 @@ int sc_mark(sc_handle* h, int32_t which);
 int sc_elapsed(sc_handle* h, float* ms);
 /* Kernel launches issued by this handle since creation (persistent + one-off). */
 int64_t sc_launches(const sc_handle* h);
-/* Diagnostics: with SCMWU_TIMING=1 in the environment, per-phase SM-cycle sums of the
- * last sc_ftp as seen by CTA 0 (9 values: pass, warp join, CTA partial, barrier 1,
- * fold, barrier 2, reduced read, control tail, tail join); zeros otherwise. */
+/* Diagnostics (builds with -DSCMWU_PHASE_TIMING and SCMWU_TIMING=1 in the environment):
+ * out[0..9) per-phase SM-cycle sums of the last sc_ftp as seen by CTA 0 (pass, warp
+ * join, CTA partial, barrier 1, fold, barrier 2, reduced read, control tail, tail join),
+ * out[9..169) each CTA's streaming cycles, out[169..329) its SM id, out[329..489) and
+ * out[489..649) global-timer ns at the start / end of its last pass, out[649..656)
+ * cycle sums of the control tail's sections (CTA 0); zeros otherwise. */
 int sc_debug_timing(sc_handle* h, double* out);
 int sc_pd_pair(sc_handle* h, double* mu /* n1 */, double* gam /* n - n1 */, double* dist);
 /* Row sharding (world > 1).  The per-pass exchange runs INSIDE the persistent kernel:

@@ -32,7 +32,9 @@
 #else
 #define SC_HD inline
 #endif
-#if defined(__CUDA_ARCH__) && defined(SCMWU_TAIL_UNROLL)
+// the O(d) loops of the tail are latency chains (smem load -> fp64 -> store); unrolling
+// overlaps them (tail 16.5k -> ~8.5k cycles at d = 100, profiles/r01_overhead.md)
+#if defined(__CUDA_ARCH__) && !defined(SCMWU_TAIL_NO_UNROLL)
 #define SC_UNROLL4 _Pragma("unroll 4")
 #else
 #define SC_UNROLL4
@@ -159,6 +161,20 @@ struct Control {
     int64_t evict_idx = -1;
     // shared-memory copy of the pending pd_counter state (device); nullptr = global
     double* pend_buf = nullptr;
+    // diagnostics (timing builds): cycle sums of the tail's sections, lane 0 of CTA 0
+    long long* tt = nullptr;
+    long long tt_prev = 0;
+    SC_HD void tmark(int i) {
+#if defined(__CUDA_ARCH__) && defined(SCMWU_PHASE_TIMING)
+        if (tt != nullptr) {
+            const long long now = clock64();
+            if (i > 0) tt[i] += now - tt_prev;
+            tt_prev = now;
+        }
+#else
+        (void)i;
+#endif
+    }
 
     // ------------------------------------------------------------ helpers
     SC_HD bool is_check(int64_t tt) const {
@@ -391,6 +407,7 @@ SC_UNROLL4
                 if (j == d + 1) v.ynew[j] = s2v;
             }
         }
+        tmark(2);
         // ---- accepted witness: y_sum += y, window push; the width check of this
         // iteration is deferred to the next pass
         const bool chk = is_check(k);
@@ -422,7 +439,9 @@ SC_UNROLL4
         t = k;
         value_prev = value;
         check_prev = chk;
+        tmark(3);
         push_window(k);
+        tmark(4);
         if (chk) {
             const double inv_len = 1.0 / (double)win_len;
 SC_UNROLL4
@@ -432,7 +451,9 @@ SC_UNROLL4
         const double m = kind == SC_SES ? red[kS_M] : red[kV_M];
         shift_pass = m;
         L::sync();
+        tmark(5);
         write_pass(pp);
+        tmark(6);
         return kPass;
     }
 
@@ -498,7 +519,9 @@ SC_UNROLL4
     // `red` reduces iterate t+1 (speculative) and the checks of iteration t.
     SC_HD int after_pass(const double* red, const double* red0, double* y_tilde,
                          PassParams* pp) {
+        tmark(0);
         int flow = finish_iteration(red, y_tilde);
+        tmark(1);
         if (flow == kStop) return kDone;
         if (flow == kContinue && t < T) return process_iterate(red, y_tilde, pp);
         // end of the rung (FTP) or of the run (REFINE)

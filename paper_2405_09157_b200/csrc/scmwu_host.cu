@@ -443,6 +443,11 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     // last-arriver 16.9 us (147 CTAs poll one line while one CTA folds), redundant worse
     p.fold_mode = kFoldTwoBarriers;
     if (const char* f = getenv("SCMWU_FOLD")) p.fold_mode = atoi(f);
+    // next-pass prefetch placement (A/B, profiles/r01_overhead.md): during the reduction
+    // (default, best by ~1%), after the reduction (SCMWU_DEFER_PREFETCH) or after the tail
+    // (SCMWU_DEFER_PREFETCH + SCMWU_FLUSH_AFTER_TAIL)
+    p.wrap_prefetch = getenv("SCMWU_DEFER_PREFETCH") ? 0 : 1;
+    p.flush_after_tail = getenv("SCMWU_FLUSH_AFTER_TAIL") ? 1 : 0;
     p.X = h->X; p.radii = h->radii; p.row_begin = h->row_begin;
     p.rho = h->prob.rho; p.inv_rho = 1.0 / h->prob.rho; p.R = h->prob.R; p.ln_r = h->prob.ln_r;
     p.D = h->prob.D; p.g1 = h->g1;
@@ -451,7 +456,10 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     h->last_alpha = args->alpha;
     p.args = *args; p.res = h->res; p.y_tilde = h->y_tilde; p.best_y = h->best_y;
     p.status = h->status; p.stage_stride = h->stage_stride; p.rad_off = h->rad_off;
-    if (!h->timing && getenv("SCMWU_TIMING")) CK(cudaMalloc(&h->timing, 16 * 8), "alloc timing");
+    if (!h->timing && getenv("SCMWU_TIMING")) {
+        CK(cudaMalloc(&h->timing, (16 + 4 * 160 + 16) * 8), "alloc timing");
+    }
+    if (h->timing) CK(cudaMemsetAsync(h->timing, 0, (16 + 4 * 160 + 16) * 8, h->stream), "timing");
     p.timing = h->timing;
     p.v1 = h->v1;
     p.world = h->prob.world;
@@ -696,10 +704,12 @@ int64_t sc_launches(const sc_handle* h) { return h ? h->launches : 0; }
 
 int sc_debug_timing(sc_handle* h, double* out) {
     if (!h || !out) return SC_EARG;
-    if (!h->timing) { for (int i = 0; i < 9; ++i) out[i] = 0.0; return SC_OK; }
-    long long t[9];
+    if (!h->timing) { for (int i = 0; i < 9 + 4 * 160 + 7; ++i) out[i] = 0.0; return SC_OK; }
+    long long t[16 + 4 * 160 + 16];
     CK(cudaMemcpy(t, h->timing, sizeof(t), cudaMemcpyDeviceToHost), "copy timing");
     for (int i = 0; i < 9; ++i) out[i] = (double)t[i];
+    for (int i = 0; i < 4 * 160; ++i) out[9 + i] = (double)t[16 + i];
+    for (int i = 0; i < 7; ++i) out[9 + 4 * 160 + i] = (double)t[16 + 4 * 160 + i];
     return SC_OK;
 }
 

@@ -132,6 +132,8 @@ struct KParams {
     int G, gP;                 // grid; SVM: CTAs [0, gP) hold P rows
     int tile_rows, stages, resident;   // rows per warp tile, stages per warp ring
     int fold_mode;                     // kFoldTwoBarriers / kFoldRedundant / kFoldLast
+    int wrap_prefetch;                 // 1: prefetch the next pass during the reduction
+    int flush_after_tail;              // 1: issue the next pass's copies after the tail
     int64_t n, n1;
     const double* X;           // n x ld (ld even, padded with zeros)
     const double* radii;       // SES: n rounded up to even (zero padded)
@@ -377,11 +379,12 @@ __host__ __device__ inline int warp_tile_count(int nwt, int w) {
 // control tail run.
 struct WarpStream {
     int cnt;          // warp tiles per pass
-    int q_next;       // local index of the next tile to issue
+    int issued;       // tiles of the current pass issued so far
+    int deferred;     // copies for the NEXT pass held back until after the reduction
     int s;            // stage of the next tile to consume
     uint32_t phase;   // parity of that stage's full barrier
     int s_issue;      // stage the next copy goes to (tiles fill stages cyclically)
-    int pending;      // tiles in flight (constant while streaming)
+    int inflight;     // issued and not yet consumed
 };
 
 __device__ __forceinline__ void issue_tile(const KParams& p, const SmemMap& m, int64_t r0,
@@ -413,9 +416,34 @@ __device__ __forceinline__ void stream_start(const KParams& p, const SmemMap& m,
     const int first = ws.cnt < p.stages ? ws.cnt : p.stages;
     if ((threadIdx.x & 31) == 0)
         for (int q = 0; q < first; ++q) issue_tile(p, m, r0, r1, w, q, q);
-    ws.pending = first;
+    ws.issued = first;
+    ws.deferred = 0;
+    ws.inflight = first;
     ws.s_issue = first % p.stages;
-    ws.q_next = ws.cnt > 0 ? first % ws.cnt : 0;
+}
+
+// Copies of the next pass are held back while the grid reduction runs: ~30 MB of
+// prefetches in flight make the barrier's L2 atomics and polls queue behind them
+// (measured: barrier 1 grew to ~23k cycles, profiles/r01_overhead.md).  They are
+// issued here, after the reduction, and overlap the control tail instead.
+__device__ __forceinline__ void stream_flush(const KParams& p, const SmemMap& m, int64_t r0,
+                                             int64_t r1, int w, WarpStream& ws) {
+    if (p.resident || ws.deferred == 0) return;
+    if (p.wrap_prefetch) {               // already issued at the end of the pass
+        ws.issued = ws.deferred;
+        ws.deferred = 0;
+        return;
+    }
+    if ((threadIdx.x & 31) == 0)
+        for (int q = 0; q < ws.deferred; ++q) {
+            issue_tile(p, m, r0, r1, w, q, ws.s_issue);
+            ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
+        }
+    else
+        ws.s_issue = (ws.s_issue + ws.deferred) % p.stages;
+    ws.issued = ws.deferred;
+    ws.inflight += ws.deferred;
+    ws.deferred = 0;
 }
 
 __device__ __forceinline__ const unsigned char* acquire_stage(const KParams& p,
@@ -435,17 +463,28 @@ __device__ __forceinline__ void release_stage(const KParams& p, const SmemMap& m
         return;
     }
     __syncwarp();
-    if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, w, ws.q_next, ws.s_issue);
-    ws.q_next = ws.q_next + 1 == ws.cnt ? 0 : ws.q_next + 1;
-    ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
+    --ws.inflight;
+    if (ws.issued < ws.cnt) {            // the next tile of this pass
+        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, w, ws.issued, ws.s_issue);
+        ++ws.issued;
+        ++ws.inflight;
+        ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
+    } else if (p.wrap_prefetch) {        // (A/B) prefetch the next pass right away
+        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, w, ws.deferred, ws.s_issue);
+        ++ws.deferred;
+        ++ws.inflight;
+        ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
+    } else {
+        ++ws.deferred;                   // a tile of the next pass: see stream_flush
+    }
     if (++ws.s == p.stages) { ws.s = 0; ws.phase ^= 1u; }
 }
 
-// before exit: the SW copies of the next pass are still in flight
+// before exit: wait for every copy still in flight
 __device__ __forceinline__ void stream_drain(const KParams& p, const SmemMap& m, int w,
                                              WarpStream& ws) {
     if (p.resident) return;
-    for (int i = 0; i < ws.pending; ++i) {
+    for (int i = 0; i < ws.inflight; ++i) {
         mbar_wait(&m.full[w * p.stages + ws.s], ws.phase);
         if (++ws.s == p.stages) { ws.s = 0; ws.phase ^= 1u; }
     }
@@ -493,7 +532,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
     const double* yprev = m.vec + dd8;
     const double* ywin = m.vec + 5 * dd8;
     bool ok[CPL];
-    double U[CPL], up[CPL], yw[CPL], Sd[CPL];
+    double U[CPL], up[CPL], Sd[CPL];   // the window average (CHECK) stays in smem
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int j = l + LPR * c;
@@ -502,7 +541,6 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         ok[c] = (FULL && c < CPL - 1) || j < d;
         U[c] = ok[c] ? ysum[j] : 0.0;
         up[c] = ok[c] ? yprev[j] : 0.0;
-        yw[c] = (CHECK && ok[c]) ? ywin[j] : 0.0;
         Sd[c] = 0.0;
     }
     const double t = pp.t, er = pp.eta_rho, al = pp.alpha, sh = pp.shift;
@@ -535,7 +573,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                     const double wv = up[c] - x;
                     sw = fma(wv, wv, sw);
                     if (CHECK) {
-                        const double yv = yw[c] - x;
+                        const double yv = ywin[l + LPR * c] - x;
                         sf = fma(yv, yv, sf);
                     }
                 }
@@ -842,6 +880,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         const int sl = p.slot_len;
         ctl.evict_buf = m.evict;
         ctl.pend_buf = m.pend;
+#ifdef SCMWU_PHASE_TIMING
+        if (p.timing != nullptr && b == 0 && lane == 0) ctl.tt = p.timing + 16 + 640;
+#endif
         ctl.s = CtlSlots{p.ring, p.ring_cap, dd8, p.slots, p.slots + sl, p.slots + 2 * sl,
                          p.slots + 4 * sl};
         for (int j = lane; j < dd8; j += 32) {
@@ -874,8 +915,18 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         tacc[i] += tnow - tprev;                     \
         tprev = tnow;                                \
     }
+#ifdef SCMWU_PHASE_TIMING
+    long long tcta = 0, tcta0 = 0;
+    unsigned long long g_start = 0, g_end = 0;
+#endif
     while (pp->action == kPass) {
         const PassParams ps = *pp;
+#ifdef SCMWU_PHASE_TIMING
+        if (tid == 0) {
+            tcta0 = clock64();
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+        }
+#endif
         if (KIND == SC_SES) {
             if (ps.check) ses_pass<LPR, CPL, NB, FULL, true>(p, m, ps, r0, r1, ws, pass_idx);
             else ses_pass<LPR, CPL, NB, FULL, false>(p, m, ps, r0, r1, ws, pass_idx);
@@ -885,6 +936,14 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         }
         SCMWU_TMARK(0)
         consumer_sync();
+#ifdef SCMWU_PHASE_TIMING
+        // per-CTA streaming time (all CTAs): the skew the first grid barrier absorbs
+        if (tid == 0 && p.timing != nullptr) {
+            const long long tnow = clock64();
+            tcta += tnow - tcta0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+        }
+#endif
         SCMWU_TMARK(1)
         // CTA partial, fixed warp order, written in the reduced layout
         const int nw_act = nwt < kNW ? nwt : kNW;   // warps that own at least one tile
@@ -987,6 +1046,10 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             consumer_sync();
             SCMWU_TMARK(6)
         }
+        // the reduction is done: release the next pass's copies (they overlap the tail);
+        // warp 0 runs the tail, so it issues its own copies after it (issuing right
+        // before the tail slowed the tail's first section 3k -> 7k cycles)
+        if (warp != 0 && !p.flush_after_tail) stream_flush(p, m, r0, r1, warp, ws);
         if (m.flags[1]) {   // a peer never arrived: give up with an exchange error
             if (b == 0 && tid == 0) *p.status = SC_ENCCL;
             break;
@@ -994,15 +1057,27 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         if (warp == 0) {
             int act = ctl.after_pass(m.red, p.red0, y_tilde, pp);
             if (lane == 0) pp->action = act;
+            stream_flush(p, m, r0, r1, warp, ws);
         }
         SCMWU_TMARK(7)
         consumer_sync();
+        if (warp != 0 && p.flush_after_tail) stream_flush(p, m, r0, r1, warp, ws);
         SCMWU_TMARK(8)
         ++pass_idx;
     }
 #undef SCMWU_TMARK
     if (timed)
         for (int i = 0; i < 9; ++i) p.timing[i] = tacc[i];
+#ifdef SCMWU_PHASE_TIMING
+    if (tid == 0 && p.timing != nullptr) {
+        p.timing[16 + b] = tcta;
+        int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.timing[16 + 160 + b] = smid;
+        p.timing[16 + 320 + b] = (long long)g_start;   // last pass, global ns clock
+        p.timing[16 + 480 + b] = (long long)g_end;
+    }
+#endif
     // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
     stream_drain(p, m, warp, ws);
     if (b == 0 && warp == 0) {

@@ -9,6 +9,8 @@ import os
 import sys
 import time
 
+import numpy as np
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2405_09157_b200 import meta, ses, svm  # noqa: E402
@@ -55,7 +57,30 @@ def main():
               f"kernel {r.kernel_ms:.1f} ms -> {us:.2f} us/pass, "
               f"{bytes_pass / us / 1e3:.1f} GB/s", flush=True)
         if os.environ.get("SCMWU_TIMING"):
-            t = dev.handle.debug_timing() / max(r.passes, 1)
+            full = dev.handle.debug_timing()
+            G = dev.handle.info()["grid"]
+            per = full[9:9 + G] / max(r.passes, 1)
+            sm = full[169:169 + G]
+            if per.max() > 0:
+                order = np.argsort(per)
+                print(f"  per-CTA streaming cycles/pass: min {per.min():.0f} median "
+                      f"{np.median(per):.0f} max {per.max():.0f}; slowest CTAs (cta:sm) "
+                      + " ".join(f"{i}:{int(sm[i])}" for i in order[-6:])
+                      + "; fastest " + " ".join(f"{i}:{int(sm[i])}" for i in order[:4]),
+                      flush=True)
+            gs, ge = full[329:329 + G], full[489:489 + G]
+            if gs.max() > 0:
+                base = gs.min()
+                print(f"  last pass, global ns: start spread {gs.max() - gs.min():.0f}, end "
+                      f"spread {ge.max() - ge.min():.0f}, CTA0 start +{gs[0] - base:.0f} end "
+                      f"+{ge[0] - base:.0f}, latest start CTA {int(np.argmax(gs))}, latest end "
+                      f"CTA {int(np.argmax(ge))} (+{ge.max() - base:.0f})", flush=True)
+            ts = full[649:656] / max(r.passes, 1)
+            if ts.sum() > 0:
+                print("  tail sections cycles/pass: finish_iteration %.0f, oracle epilogue %.0f,"
+                      " update loops %.0f, window %.0f, checks+shift %.0f, write_pass %.0f"
+                      % tuple(ts[1:7]), flush=True)
+            t = full[:9] / max(r.passes, 1)
             names = ["pass", "join", "cta_part", "bar1", "fold", "bar2", "red_read", "tail",
                      "tail_join"]
             tot = t.sum()
