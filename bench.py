@@ -47,6 +47,16 @@ WORKLOADS = {
                    desc="SES n=10^4 d=10 Gaussian, eps=1e-2 (configs[0])"),
     "ses_c4": dict(kind="ses", n=10 ** 7, d=100, dist="uniform-ball", seed=0, eps=1e-3,
                    desc="SES n=10^7 d=100 uniform-in-ball, eps=1e-3 (configs[3])"),
+    # drawn on the device (devgen, sc_create_generated): no host copy of X exists
+    "ses_c4_gen": dict(kind="ses", n=10 ** 7, d=100, dist="uniform-ball", seed=0, eps=1e-3,
+                       generated=True,
+                       desc="SES n=10^7 d=100 uniform-in-ball, eps=1e-3 (configs[3]), "
+                            "generated on the device"),
+    "svm_c5_gen": dict(kind="svm", n1=10 ** 7, n2=10 ** 7, d=512, seed=0, gap=1.0, eps=1e-3,
+                       generated=True, horizon=64,
+                       desc="SVM n=2x10^7 d=512 gap 1 (configs[4], 81.9 GB fp64), generated "
+                            "on the device; per-iteration HBM GB/s over a 64-iteration "
+                            "refine run"),
 }
 # GPU iteration counts of full solves measured by this bench (profiles/); used only by the
 # reference arm to extrapolate the CPU port's s/iter to a time-to-eps.
@@ -186,6 +196,8 @@ def cpu_sample(w, inst, max_seconds=20.0, max_iters=100_000):
 def reference_arm(args, w, rank):
     if rank != 0:
         return
+    if w.get("generated"):
+        return reference_arm_scaled(args, w)
     inst = make_instance(w)
     t0 = time.perf_counter()
     samples = []
@@ -211,6 +223,50 @@ def reference_arm(args, w, rank):
         "wall_s": time.perf_counter() - t0,
     }
     print(json.dumps(line), flush=True)
+
+
+def reference_arm_scaled(args, w):
+    """Reference arm of the device-generated workloads: the host cannot hold these
+    instances (C5 is 82 GB), so each step times the oracle port on a row sample and scales
+    per-iteration time linearly to the full row count."""
+    t0 = time.perf_counter()
+    ws = _sample_cfg(w)
+    warm = make_instance(ws)
+    for _ in range(args.warmup):
+        cpu_sample(ws, warm, max_seconds=1.0, max_iters=1)
+    spis = []
+    for _ in range(args.steps):
+        spi, desc = cpu_scaled(w, 20.0)
+        spis.append(spi)
+    spi = statistics.median(spis)
+    bpp = alg_bytes_per_pass(w)
+    if w.get("horizon") is not None:
+        value, metric, unit, hib = bpp / spi / 1e9, "per-iteration HBM GB/s", "GB/s", True
+    else:
+        iters = ITERS_EST.get(args.workload.replace("_gen", ""), 0)
+        value, metric, unit, hib = spi * iters, "time-to-eps (s)", "s", False
+        desc += f"; x {iters} iterations (the GPU solve's count; extrapolated)"
+    line = {
+        "impl": "reference", "metric": metric, "value": value, "unit": unit,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": spi * 1000.0, "higher_is_better": hib, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w["desc"], "eps": w["eps"], "seed": w["seed"]},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": 1, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _sample_cfg(w):
+    ws = dict(w)
+    if w["kind"] == "ses":
+        ws["n"] = min(w["n"], 2_000)
+    else:
+        ws["n1"], ws["n2"] = min(w["n1"], 1_000), min(w["n2"], 1_000)
+    return ws
 
 
 # ------------------------------------------------------------------ our arm
@@ -354,6 +410,173 @@ def our_arm(args, w, rank, world):
         tdist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ device-generated workloads
+def gen_device(w, comm, local):
+    from paper_2405_09157_b200 import devgen
+    if w["kind"] == "ses":
+        return devgen.gen_ses_device(w["n"], w["d"], w["seed"], w["dist"], device=local,
+                                     comm=comm)
+    return devgen.gen_svm_device(w["n1"], w["n2"], w["d"], w["seed"], w["gap"], device=local,
+                                 comm=comm)
+
+
+def fixed_run(w, inst):
+    """One refine_run of exactly w['horizon'] iterations (stopping disabled) at the
+    feasible end of the range, so it never separates: a fixed amount of streaming work."""
+    from paper_2405_09157_b200 import meta
+    dev = inst.dev
+    if w["kind"] == "ses":
+        spec = meta.OracleSpec(dev.cone, 3.0 * inst.D / math.sqrt(2.0), w["d"] + 1, dev,
+                               math.sqrt(2.0), meta.Orientation.MAX)
+        alpha = inst.D
+    else:
+        spec = meta.OracleSpec(dev.cone, 2.0 * inst.D, w["d"] + 2, dev, 2.0,
+                               meta.Orientation.MIN, counter_progress=True)
+        alpha = 1e-3 * inst.D
+    return meta.refine_run(spec, alpha, w["horizon"], meta.EarlyStopConfig(enabled=False),
+                           dev.progress)
+
+
+def gen_arm(args, w, rank, world):
+    import torch
+    dist = world > 1
+    comm = None
+    if dist:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        from paper_2405_09157_b200 import shard
+        comm = shard.Comm()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    fixed = w.get("horizon") is not None
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            tdist.barrier()
+
+    def vmax(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step(inst):
+        return fixed_run(w, inst) if fixed else solve(w, inst)
+
+    t0 = time.perf_counter()
+    inst = gen_device(w, comm, local)
+    gen_s = time.perf_counter() - t0
+    h = inst.dev.handle
+    info = h.info()
+    for _ in range(args.warmup):
+        step(inst)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    l0 = h.launches()
+    times, outs = [], []
+    for _ in range(args.steps):
+        h.mark(0)
+        outs.append(step(inst))
+        h.mark(1)
+        times.append(h.elapsed_ms() / 1000.0)
+    barrier()
+    launches = h.launches() - l0
+    clk = clocks.stop()
+    t_step = vmax(max(times))
+    if fixed:
+        kernel_s = sum(r.kernel_ms for r in outs) / 1000.0
+        passes = sum(r.passes for r in outs)
+        iters = outs[-1].iterations
+    else:
+        kernel_s = sum(r.kernel_ms for r, _ in outs) / 1000.0
+        passes = sum(r.passes for r, _ in outs)
+        iters = outs[-1][0].total_iterations
+    inst.close()
+    # e2e through the public API: generate on the device + the step, host results read back
+    barrier()
+    t0 = time.perf_counter()
+    inst_e = gen_device(w, comm, local)
+    out_e = step(inst_e)
+    inst_e.close()
+    torch.cuda.synchronize()
+    e2e_s = vmax(time.perf_counter() - t0)
+    bpp = alg_bytes_per_pass(w)
+    peak, peak_kind = measured_peak()
+    achieved = passes * bpp / kernel_s / 1e9 if kernel_s > 0 else 0.0
+    if fixed:
+        # per-iteration HBM throughput of the whole job (all ranks' rows)
+        value = passes / args.steps * bpp / t_step / 1e9
+        metric, unit, hib = "per-iteration HBM GB/s", "GB/s", True
+        e2e_v = passes / args.steps * bpp / e2e_s / 1e9
+        sd = w["d"] + (1 if w["kind"] == "ses" else 2)
+        d2h = 2 * sd * 8
+    else:
+        value, metric, unit, hib, e2e_v = t_step, "time-to-eps (s)", "s", False, e2e_s
+        rep_e = out_e[0]
+        d2h = (w["d"] + 2) * 8 * 2 * rep_e.search_steps + 8 * 4
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_pass")
+        except (OSError, ValueError):
+            traffic = None
+    line = {
+        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_step * 1000.0, "higher_is_better": hib,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, drawn on the device (Philox; same distribution as gen_ses/gen_svm)",
+        "config": {"workload": w["desc"], "eps": w["eps"], "seed": w["seed"],
+                   "parallelism": (f"row-sharded x{world} (in-kernel NVLink exchange)"
+                                   if world > 1 else "1 GPU"),
+                   "iterations": iters, "generate_s": gen_s,
+                   "l2": "inputs larger than L2 (X = %.0f MB)" % (bpp / 1e6), "kernel": info},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "alg_bytes_per_pass": bpp,
+                     "us_per_pass": kernel_s / passes * 1e6 if passes else None,
+                     "kernel_s": kernel_s, "passes": passes},
+        "e2e": {"value": e2e_v, "unit": unit, "h2d_bytes_per_step":
+                8 * w["d"] if w["kind"] == "svm" else 0, "d2h_bytes_per_step": int(d2h),
+                "note": "generation on the device + the step; X never exists on the host"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        spi, desc = cpu_scaled(w, args.cpu_seconds)
+        cv = bpp / spi / 1e9 if fixed else spi * iters
+        line["cpu_baseline"] = {"value": cv, "unit": unit, "cores": 1, "kind": "port",
+                                "sample": desc + (f"; x {iters} GPU iterations" if not fixed
+                                                  else "; GB/s = algorithmic bytes / s")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        tdist.destroy_process_group()
+
+
+def cpu_scaled(w, seconds):
+    """Seconds per MWU iteration of the oracle port at the workload's FULL size, measured
+    on a row sample (numpy generation of the same distribution) and scaled linearly in the
+    number of rows (each iteration is one pass over them)."""
+    ws = dict(w)
+    if w["kind"] == "ses":
+        ws["n"] = min(w["n"], 100_000)
+        factor = w["n"] / ws["n"]
+    else:
+        ws["n1"] = min(w["n1"], 50_000)
+        ws["n2"] = min(w["n2"], 50_000)
+        factor = (w["n1"] + w["n2"]) / (ws["n1"] + ws["n2"])
+    s = cpu_sample(ws, make_instance(ws), max_seconds=seconds)
+    rows = ws["n"] if w["kind"] == "ses" else ws["n1"] + ws["n2"]
+    return s["s_per_iter"] * factor, (
+        f"{s['iters']} MWU iterations (one refine_run) of the oracle port on a {rows}-row "
+        f"sample of the same distribution, {s['s_per_iter']:.4f} s/iter scaled x{factor:g} to "
+        f"the full row count")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -369,6 +592,8 @@ def main():
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
         reference_arm(args, w, rank)
+    elif w.get("generated"):
+        gen_arm(args, w, rank, world)
     else:
         our_arm(args, w, rank, world)
 

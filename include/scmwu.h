@@ -125,6 +125,30 @@ typedef struct {
  * holds all n rows; radii must be NULL. */
 int sc_create(const sc_problem* prob, const double* X, const double* X_tail,
               const double* radii, sc_handle** out);
+/* On-device synthetic instances: the same distributions as
+ * instances.gen_ses / gen_svm (R/instances.py:155-199), drawn with a counter-based
+ * Philox4x32-10 keyed by (seed, GLOBAL row index), so every shard generates its own rows
+ * and the instance does not depend on the sharding.  Not the bits of numpy's PCG64:
+ * only the distribution matches.  X never exists on the host. */
+enum sc_gen_dist { SC_GEN_GAUSSIAN = 0, SC_GEN_UNIFORM_BALL = 1, SC_GEN_SPHERE_SURFACE = 2,
+                   SC_GEN_SVM_CLUSTERS = 3 };
+typedef struct {
+    int32_t dist;               /* an sc_gen_dist value: SES 0-2, SVM 3 */
+    uint64_t seed;
+    double gap;                 /* SVM: cluster gap */
+    const double* direction;    /* SVM: unit separating direction (d values, host) */
+} sc_gen;
+/* prob->D / rho / R / rank / ln_r are filled in by the call (D computed on the device:
+ * SES max_i |v_1 - v_i|, SVM max_i |x_i|, over THIS shard's rows; sharded callers reduce
+ * the shards' D with max and hand it to sc_set_range).  v1_out (SES, d values: the global
+ * row 0, drawn by every shard) may be NULL. */
+int sc_create_generated(sc_problem* prob, const sc_gen* gen, double* v1_out,
+                        sc_handle** out);
+/* Set the range D; rho, R, rank and ln_r follow as in the solvers (R/ses.py:161,169,
+ * R/svm.py:168,186). */
+int sc_set_range(sc_handle* h, double D);
+/* Copy `count` resident rows starting at local row `first` to out (count x d, row-major). */
+int sc_read_rows(sc_handle* h, int64_t first, int64_t count, double* out);
 int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
            double* y_tilde /* dual_dim */, double* best_y /* dual_dim */);
 int sc_progress(sc_handle* h, const double* y /* d values */, double* f);

@@ -44,6 +44,16 @@ class ScProblem(ctypes.Structure):
                 ("n_local", ctypes.c_int64), ("n1_local", ctypes.c_int64)]
 
 
+SC_GEN_GAUSSIAN, SC_GEN_UNIFORM_BALL, SC_GEN_SPHERE_SURFACE, SC_GEN_SVM_CLUSTERS = 0, 1, 2, 3
+GEN_DISTS = {"gaussian": SC_GEN_GAUSSIAN, "uniform-ball": SC_GEN_UNIFORM_BALL,
+             "sphere-surface": SC_GEN_SPHERE_SURFACE}
+
+
+class ScGen(ctypes.Structure):
+    _fields_ = [("dist", ctypes.c_int32), ("seed", ctypes.c_uint64), ("gap", ctypes.c_double),
+                ("direction", ctypes.POINTER(ctypes.c_double))]
+
+
 class ScFtpArgs(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("has_progress", ctypes.c_int32),
                 ("alpha", ctypes.c_double), ("eps", ctypes.c_double),
@@ -69,7 +79,8 @@ class ScFtpResult(ctypes.Structure):
 EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "sc_pd_pair",
            "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_debug_timing",
            "sc_local_red0", "sc_progress_parts", "sc_set_globals", "sc_ipc_handle",
-           "sc_connect", "sc_last_error", "sc_destroy", "sc_version")
+           "sc_connect", "sc_last_error", "sc_destroy", "sc_version", "sc_create_generated",
+           "sc_set_range", "sc_read_rows")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -115,7 +126,40 @@ class Engine:
         lib.sc_set_globals.argtypes = [vp, _dp, _dp, ctypes.c_double]
         lib.sc_ipc_handle.argtypes = [vp, ctypes.c_char_p]
         lib.sc_connect.argtypes = [vp, ctypes.c_char_p]
+        lib.sc_create_generated.argtypes = [ctypes.POINTER(ScProblem), ctypes.POINTER(ScGen),
+                                            _dp, ctypes.POINTER(vp)]
+        lib.sc_set_range.argtypes = [vp, ctypes.c_double]
+        lib.sc_read_rows.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, _dp]
         self.lib = lib
+
+    def create_generated(self, kind: int, n: int, d: int, seed: int, dist: int,
+                         n1: int = 0, gap: float = 1.0, direction=None, grid: int = 0,
+                         device: int = 0, shard: Optional[tuple] = None
+                         ) -> tuple["Handle", float, Optional[np.ndarray]]:
+        """Draw the instance on the device (sc_create_generated).  ``shard = (world, index,
+        row0, n_local)``.  Returns (handle, this shard's range D, SES anchor row v1)."""
+        world, index, row0, n_local = 1, 0, 0, n
+        if shard is not None and shard[0] > 1:
+            world, index, row0, n_local = shard
+        n1_local = max(0, min(n_local, n1 - row0)) if kind == SC_SVM else 0
+        prob = ScProblem(kind=kind, d=d, n=n, n1=n1, grid=grid, device=device, world=world,
+                         shard=index, row0=row0, n_local=n_local, n1_local=n1_local)
+        dvec = None
+        if direction is not None:
+            dvec = np.ascontiguousarray(direction, dtype=np.float64)
+        gen = ScGen(dist=dist, seed=seed, gap=gap, direction=_ptr(dvec))
+        v1 = np.zeros(d) if kind == SC_SES else None
+        h = ctypes.c_void_p()
+        st = self.lib.sc_create_generated(ctypes.byref(prob), ctypes.byref(gen), _ptr(v1),
+                                          ctypes.byref(h))
+        if st != SC_OK:
+            msg = self.lib.sc_last_error(h).decode() if h.value else "sc_create_generated failed"
+            if h.value:
+                self.lib.sc_destroy(h)
+            if st == SC_ECUDA:
+                raise NativeUnavailable(f"CUDA engine cannot run: {msg}")
+            raise NativeError(st, msg)
+        return Handle(self, h, prob), float(prob.D), v1
 
     def create(self, kind: int, X, X_tail, radii, D: float, rho: float, R: float,
                rank: int, n1: int = 0, grid: int = 0, device: int = 0,
@@ -237,6 +281,18 @@ class Handle:
         v = None if v1 is None else np.ascontiguousarray(v1, dtype=np.float64)
         self._check(self.engine.lib.sc_set_globals(self.h, _ptr(red0), _ptr(v), g1),
                     "sc_set_globals")
+
+    def set_range(self, D: float) -> None:
+        self._check(self.engine.lib.sc_set_range(self.h, D), "sc_set_range")
+        self.prob.D = D
+
+    def read_rows(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
+        if count is None:
+            count = self.prob.n_local - first
+        out = np.zeros((count, self.d))
+        self._check(self.engine.lib.sc_read_rows(self.h, first, count, _ptr(out)),
+                    "sc_read_rows")
+        return out
 
     def progress_parts(self, y) -> np.ndarray:
         y = np.ascontiguousarray(np.asarray(y, dtype=np.float64)[: self.d])

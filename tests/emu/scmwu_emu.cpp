@@ -312,6 +312,25 @@ int sc_local_red0(sc_handle* h, double* out) {
     return SC_OK;
 }
 
+// on-device generation has no CPU counterpart: the emulator only exports the symbol
+int sc_create_generated(sc_problem*, const sc_gen*, double*, sc_handle** out) {
+    if (out) *out = nullptr;
+    return SC_EARG;
+}
+
+int sc_set_range(sc_handle* h, double D) {
+    if (!h || !(D >= 0.0)) return SC_EARG;
+    h->prob.D = D;
+    return SC_OK;
+}
+
+int sc_read_rows(sc_handle* h, int64_t first, int64_t count, double* out) {
+    if (!h || !out || first < 0 || count < 0 || first + count > h->prob.n_local) return SC_EARG;
+    const int d = h->prob.d;
+    std::copy(h->X.begin() + first * d, h->X.begin() + (first + count) * d, out);
+    return SC_OK;
+}
+
 int sc_set_globals(sc_handle* h, const double* red0, const double* v1, double g1) {
     if (!h || !red0) return SC_EARG;
     std::copy(red0, red0 + h->red0.size(), h->red0.begin());
