@@ -76,6 +76,7 @@ struct PassParams {
     double S1, S2;     // SVM: sums of s1, s2
     double s1p, s2p;   // SVM: s1, s2 of iteration k-1
     int check;         // iteration k-1 is a check iteration (window / counter)
+    int width;         // SES: the width check of iteration k-1 needs the exact residuals
     int action;        // 0 = pass, 1 = done
 };
 
@@ -143,6 +144,7 @@ struct Control {
     double value_prev;       // oracle value of iteration t
     double dist_prev;        // SVM counter distance of iteration t (if check)
     bool check_prev;
+    bool width_prev;         // SES: iteration t's width check needs the exact residuals
     // SVM pd bookkeeping
     bool has_counter_min; double counter_min;
     // latest iterate state (for p)
@@ -427,14 +429,37 @@ SC_UNROLL4
             if (pend_buf != nullptr) keep_state(pend_buf, v.ysum, cur);
         }
         double* slot = s.ring + (win_count % s.ring_cap) * s.ring_stride;
+        // SES width bound: with u_k = U_k / k the running average,
+        //   |alpha - g_i| + |y_k - v_i| <= |alpha| + F(u_k) + |y_k - u_k|,
+        //   F(u_k) <= F(u_{k-1}) + |u_k - u_{k-1}|,
+        // and F(u_{k-1}) = max_i |u_{k-1} - v_i| + g_i is red[kS_F] of the pass that
+        // produced this iterate.  When the bound is below the width rho the exact
+        // residuals of y_k are not needed: the check cannot fail.
+        const bool bound_ses = kind == SC_SES && k >= 2;
+        const double inv_k = 1.0 / (double)k, inv_km1 = bound_ses ? 1.0 / (double)(k - 1) : 0.0;
+        double du2 = 0.0, dy2 = 0.0;
 SC_UNROLL4
         for (int j = ln; j < dd; j += nl) {
             const double y = v.ynew[j];
-            v.pU[j] = v.ysum[j];
-            v.ysum[j] += y;
+            const double u0 = v.ysum[j];
+            v.pU[j] = u0;
+            const double u1 = u0 + y;
+            v.ysum[j] = u1;
             v.yprev[j] = y;
             if (writer) slot[j] = y;
             v.wsum[j] += y;
+            if (bound_ses && j < d) {
+                const double ub = u1 * inv_k;
+                const double du = ub - u0 * inv_km1, dy = y - ub;
+                du2 = fma(du, du, du2);
+                dy2 = fma(dy, dy, dy2);
+            }
+        }
+        width_prev = true;
+        if (bound_ses) {
+            L::sum2(du2, dy2);
+            const double wb = (fabs(a.alpha) + red[kS_F] + sqrt(du2) + sqrt(dy2)) / kSqrt2;
+            width_prev = !(wb * inv_rho <= (1.0 + kLossSlack) * (1.0 - 1e-9));
         }
         t = k;
         value_prev = value;
@@ -508,6 +533,7 @@ SC_UNROLL4
         pp->eta_rho = eta * inv_rho;
         pp->shift = shift_pass;
         pp->check = check_prev ? 1 : 0;
+        pp->width = width_prev ? 1 : 0;
         if (kind == SC_SVM) {
             pp->S1 = v.ysum[d]; pp->S2 = v.ysum[d + 1];
             pp->s1p = v.yprev[d]; pp->s2p = v.yprev[d + 1];

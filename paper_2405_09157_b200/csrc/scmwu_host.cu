@@ -227,6 +227,7 @@ KernelFn scmwu_lookup_4(int kind, int lpr, int cpl, int nb, bool full);
 KernelFn scmwu_lookup_5(int kind, int lpr, int cpl, int nb, bool full);
 KernelFn scmwu_lookup_6(int kind, int lpr, int cpl, int nb, bool full);
 KernelFn scmwu_lookup_7(int kind, int lpr, int cpl, int nb, bool full);
+KernelFn scmwu_lookup_8(int kind, int lpr, int cpl, int nb, bool full);
 }  // namespace scmwu
 
 // full: every column slot but the last is in range (d > lpr * (cpl - 1)); instantiated
@@ -235,7 +236,8 @@ static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb, bool full) {
     KernelFn (*fns[])(int, int, int, int, bool) = {scmwu_lookup_0, scmwu_lookup_1,
                                                    scmwu_lookup_2, scmwu_lookup_3,
                                                    scmwu_lookup_4, scmwu_lookup_5,
-                                                   scmwu_lookup_6, scmwu_lookup_7};
+                                                   scmwu_lookup_6, scmwu_lookup_7,
+                                                   scmwu_lookup_8};
     for (auto f : fns)
         if (KernelFn k = f(kind, lpr, cpl, nb, full)) return k;
     return nullptr;
@@ -432,6 +434,11 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
     const int d = prob->d;
     const int64_t n = P.n_local;   // rows resident on this GPU
     if (!pick_cfg(d, h->cfg)) { h->err = "d > 512 is not supported yet"; return SC_EARG; }
+    if (const char* cfg = getenv("SCMWU_CFG")) {   // A/B: "lanes,cols,groups"
+        LaunchCfg c{};
+        if (sscanf(cfg, "%d,%d,%d", &c.lpr, &c.cpl, &c.nb) == 3 && c.lpr * c.cpl >= d)
+            h->cfg = c;
+    }
     const bool full = prob->kind == SC_SES && d > h->cfg.lpr * (h->cfg.cpl - 1);
     h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl, h->cfg.nb, full);
     if (!h->fn) { h->err = "no kernel instantiated for this d"; return SC_EARG; }

@@ -518,13 +518,17 @@ __device__ __forceinline__ void reduce_scatter(double (&v)[V][NB], int l) {
 }
 
 // --------------------------------------------------------------------------------------
-// consumer pass over this warp's tiles: SES
-template <int LPR, int CPL, int NB, bool FULL, bool CHECK>
+// consumer pass over this warp's tiles: SES.  MODE 0: iterate only (the control tail
+// certified the width check of iteration k-1 by a bound); 1: + the exact
+// width residuals; 2: + the window-average progress (check iterations).
+template <int LPR, int CPL, int NB, bool FULL, int MODE>
 __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& pp,
                          int64_t r0, int64_t r1, WarpStream& ws, int pass_idx) {
+    constexpr bool CHECK = MODE == 2;
+    constexpr bool WIDTH = MODE >= 1;
     constexpr int RPW = 32 / LPR;
     constexpr int DUP = LPR / NB;
-    constexpr int NV = CHECK ? 4 : 3;
+    constexpr int NV = 2 + (WIDTH ? 1 : 0) + (CHECK ? 1 : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
     const int d = p.d, ld = p.ld, dd8 = dd8_of(p.dd);
@@ -532,7 +536,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
     const double* yprev = m.vec + dd8;
     const double* ywin = m.vec + 5 * dd8;
     bool ok[CPL];
-    double U[CPL], up[CPL], Sd[CPL];   // the window average (CHECK) stays in smem
+    double U[CPL], up[WIDTH ? CPL : 1], Sd[CPL];   // the window average (CHECK) stays in smem
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
         const int j = l + LPR * c;
@@ -540,7 +544,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         // guards fold away at compile time (-4% on the C2 pass, profiles/r01_overhead.md)
         ok[c] = (FULL && c < CPL - 1) || j < d;
         U[c] = ok[c] ? ysum[j] : 0.0;
-        up[c] = ok[c] ? yprev[j] : 0.0;
+        if (WIDTH) up[WIDTH ? c : 0] = ok[c] ? yprev[j] : 0.0;
         Sd[c] = 0.0;
     }
     const double t = pp.t, er = pp.eta_rho, al = pp.alpha, sh = pp.shift;
@@ -570,15 +574,18 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                     const double df = fma(-t, x, U[c]);
                     sa = fma(df, df, sa);
                     sl = fma(x, df, sl);
-                    const double wv = up[c] - x;
-                    sw = fma(wv, wv, sw);
+                    if (WIDTH) {
+                        const double wv = up[WIDTH ? c : 0] - x;
+                        sw = fma(wv, wv, sw);
+                    }
                     if (CHECK) {
                         const double yv = ywin[l + LPR * c] - x;
                         sf = fma(yv, yv, sf);
                     }
                 }
             }
-            v[0][k] = sa; v[1][k] = sl; v[2][k] = sw;
+            v[0][k] = sa; v[1][k] = sl;
+            if (WIDTH) v[WIDTH ? 2 : 0][k] = sw;
             if (CHECK) v[NV - 1][k] = sf;
         }
         reduce_scatter<LPR, NB, NV>(v, l);
@@ -603,7 +610,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                     Lin = fma(cc, v[1][0], Lin);
                     Rad = fma(g, A + B, Rad);
                     M = fmax(M, lp);
-                    Wd = fmax(Wd, (fabs(al - g) + sqrt(v[2][0])) * kInvSqrt2);
+                    if (WIDTH) Wd = fmax(Wd, (fabs(al - g) + sqrt(v[WIDTH ? 2 : 0][0])) * kInvSqrt2);
                 }
             }
         }
@@ -928,8 +935,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         }
 #endif
         if (KIND == SC_SES) {
-            if (ps.check) ses_pass<LPR, CPL, NB, FULL, true>(p, m, ps, r0, r1, ws, pass_idx);
-            else ses_pass<LPR, CPL, NB, FULL, false>(p, m, ps, r0, r1, ws, pass_idx);
+            if (ps.check) ses_pass<LPR, CPL, NB, FULL, 2>(p, m, ps, r0, r1, ws, pass_idx);
+            else if (ps.width) ses_pass<LPR, CPL, NB, FULL, 1>(p, m, ps, r0, r1, ws, pass_idx);
+            else ses_pass<LPR, CPL, NB, FULL, 0>(p, m, ps, r0, r1, ws, pass_idx);
         } else {
             if (ps.check) svm_pass<LPR, CPL, NB, FULL, true>(p, m, ps, r0, r1, ws, pass_idx, isP);
             else svm_pass<LPR, CPL, NB, FULL, false>(p, m, ps, r0, r1, ws, pass_idx, isP);
