@@ -230,8 +230,10 @@ KernelFn scmwu_lookup_7(int kind, int lpr, int cpl, int nb, bool full);
 KernelFn scmwu_lookup_8(int kind, int lpr, int cpl, int nb, bool full);
 }  // namespace scmwu
 
-// full: every column slot but the last is in range (d > lpr * (cpl - 1)); instantiated
-// for SES only (measured: no gain for SVM)
+// full: every column slot but the last is in range (d > lpr * (cpl - 1)), so only the last
+// slot needs a runtime guard.  Instantiated for every SES config and for the SVM configs of
+// the BASELINE dimensions; a full request falls back to the guarded kernel (correct for
+// any d).
 static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb, bool full) {
     KernelFn (*fns[])(int, int, int, int, bool) = {scmwu_lookup_0, scmwu_lookup_1,
                                                    scmwu_lookup_2, scmwu_lookup_3,
@@ -240,6 +242,7 @@ static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb, bool full) {
                                                    scmwu_lookup_8};
     for (auto f : fns)
         if (KernelFn k = f(kind, lpr, cpl, nb, full)) return k;
+    if (full) return kernel_lookup(kind, lpr, cpl, nb, false);
     return nullptr;
 }
 
@@ -439,7 +442,7 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
         if (sscanf(cfg, "%d,%d,%d", &c.lpr, &c.cpl, &c.nb) == 3 && c.lpr * c.cpl >= d)
             h->cfg = c;
     }
-    const bool full = prob->kind == SC_SES && d > h->cfg.lpr * (h->cfg.cpl - 1);
+    const bool full = d > h->cfg.lpr * (h->cfg.cpl - 1);
     h->fn = kernel_lookup(prob->kind, h->cfg.lpr, h->cfg.cpl, h->cfg.nb, full);
     if (!h->fn) { h->err = "no kernel instantiated for this d"; return SC_EARG; }
     h->dd = prob->kind == SC_SES ? d + 1 : d + 2;
