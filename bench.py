@@ -335,6 +335,7 @@ def our_arm(args, w, rank, world):
         t_step = float(t.item())
     kernel_s = sum(r.kernel_ms for r, _ in reports) / 1000.0
     passes = sum(r.passes for r, _ in reports)
+    width_passes = sum(r.width_passes for r, _ in reports)
     dev.close()
 
     # e2e: public API from host arrays (upload + download inside the timed region)
@@ -392,7 +393,8 @@ def our_arm(args, w, rank, world):
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_pass": alg_bytes_per_pass(w),
                      "us_per_pass": kernel_s / passes * 1e6 if passes else None,
-                     "kernel_s": kernel_s, "passes": passes},
+                     "kernel_s": kernel_s, "passes": passes,
+                     "exact_width_passes": width_passes},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),

@@ -118,6 +118,8 @@ typedef struct {
     /* device-side timing and work accounting of this call */
     int64_t passes;           /* streaming passes over X executed */
     float kernel_ms;          /* CUDA-event time of the persistent kernel */
+    int64_t width_passes;     /* SES: passes that evaluated the exact width residuals (the
+                                 others were certified by the bound of DESIGN.md §4.4) */
 } sc_ftp_result;
 
 /* X: row-major host rows.  SES: n rows (centres), radii n values.  SVM: the n1

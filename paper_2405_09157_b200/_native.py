@@ -73,7 +73,8 @@ class ScFtpResult(ctypes.Structure):
                 ("best_counter", ctypes.c_double), ("width_iteration", ctypes.c_int64),
                 ("width_norm", ctypes.c_double), ("has_counter_min", ctypes.c_int32),
                 ("counter_min", ctypes.c_double), ("sep_dist", ctypes.c_double),
-                ("passes", ctypes.c_int64), ("kernel_ms", ctypes.c_float)]
+                ("passes", ctypes.c_int64), ("kernel_ms", ctypes.c_float),
+                ("width_passes", ctypes.c_int64)]
 
 
 EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "sc_pd_pair",
@@ -194,7 +195,8 @@ class FtpOut:
 
     __slots__ = ("status", "kind", "reason", "iterations", "eps_eff", "value", "oracle_value",
                  "best_f", "best_counter", "y_tilde", "best_y", "width_iteration",
-                 "width_norm", "counter_min", "sep_dist", "passes", "kernel_ms", "has_claim_y")
+                 "width_norm", "counter_min", "sep_dist", "passes", "kernel_ms", "has_claim_y",
+                 "width_passes")
 
 
 class Handle:
@@ -238,6 +240,7 @@ class Handle:
         o.sep_dist = res.sep_dist
         o.passes = int(res.passes)
         o.kernel_ms = float(res.kernel_ms)
+        o.width_passes = int(res.width_passes)
         return o
 
     def progress(self, y) -> float:

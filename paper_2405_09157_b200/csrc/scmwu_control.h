@@ -51,6 +51,47 @@ constexpr double kValueTrendDrop = 0.05;
 constexpr double kLossSlack = 1e-9;
 constexpr double kSqrt2 = 1.4142135623730951;
 
+// ---- branch-free exp ---------------------------------------------------------
+// The streaming passes evaluate one (SVM) or two (SES) exponentials per row with
+// arguments down to ~-10^3 (the lagged shift keeps them <= ~0).  The CUDA libm exp takes
+// a divergent slow path near underflow, so CTAs whose rows sit in that range fell behind
+// the others (SVM C3: per-CTA pass time 190k..246k cycles, profiles/r01_overhead.md).
+// sc_exp: Cody-Waite reduction by ln 2, degree-13 Taylor polynomial of e^r on
+// |r| <= ln2/2 in Estrin form (4 dependent FMA levels instead of 13), 2^k applied as two
+// normal powers of two so gradual underflow needs no branch.  Within 2 ulp of exp()
+// (tests/test_math.py); results below 2^-1075 flush to 0.
+SC_HD double pow2i(int e) {   // 2^e for e in [-1022, 1023]
+#if defined(__CUDA_ARCH__)
+    return __hiloint2double((e + 1023) << 20, 0);
+#else
+    const uint64_t b = (uint64_t)(e + 1023) << 52;
+    double r;
+    __builtin_memcpy(&r, &b, 8);
+    return r;
+#endif
+}
+
+SC_HD double sc_exp(double x) {
+    x = fmin(fmax(x, -745.5), 709.75);
+    const double kd = rint(x * 1.4426950408889634);
+    double r = fma(-kd, 6.93147180369123816490e-01, x);   // ln2 hi (32 trailing zero bits)
+    r = fma(-kd, 1.90821492927058770002e-10, r);         // ln2 lo
+    const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+    const double q0 = fma(r, 1.0, 1.0);
+    const double q1 = fma(r, 1.0 / 6.0, 0.5);
+    const double q2 = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    const double q3 = fma(r, 1.0 / 5040.0, 1.0 / 720.0);
+    const double q4 = fma(r, 1.0 / 362880.0, 1.0 / 40320.0);
+    const double q5 = fma(r, 1.0 / 39916800.0, 1.0 / 3628800.0);
+    const double q6 = fma(r, 1.0 / 6227020800.0, 1.0 / 479001600.0);
+    const double w0 = fma(q1, r2, q0), w1 = fma(q3, r2, q2), w2 = fma(q5, r2, q4);
+    const double z0 = fma(w1, r4, w0), z1 = fma(q6, r4, w2);
+    const double p = fma(z1, r8, z0);
+    const int k = (int)kd;
+    const int k1 = k >> 1;
+    return (p * pow2i(k1)) * pow2i(k - k1);
+}
+
 // ---- layout of one reduced pass vector ------------------------------------
 // SES: T, Lin, Rad, M (max lambda+), F (max progress of U/t), Wd (max residual
 //      eigen-magnitude of iteration t), Fw (max progress of the window avg),

@@ -57,8 +57,8 @@ __global__ void iterate_kernel(const double* X, const double* radii, int64_t n, 
         const double ra = sqrt(a);
         const double nrm = er * ra;
         const double x0 = -(er * st.t) * (alpha - g);
-        const double A = exp((x0 + nrm) * kInvSqrt2 - st.shift);
-        const double B = exp((x0 - nrm) * kInvSqrt2 - st.shift);
+        const double A = sc_exp((x0 + nrm) * kInvSqrt2 - st.shift);
+        const double B = sc_exp((x0 - nrm) * kInvSqrt2 - st.shift);
         const double cc = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
         double* o = out + (i - first) * (d + 1);
         for (int j = 0; j < d; ++j) {
@@ -73,7 +73,7 @@ __global__ void iterate_kernel(const double* X, const double* radii, int64_t n, 
         for (int j = 0; j < d; ++j) s = fma(x[j], slot[j], s);
         const bool P = i < n1;
         const double lg = -er * ((P ? 1.0 : -1.0) * s - (P ? slot[d] : slot[d + 1]));
-        out[i] = exp(lg - st.shift) / st.T;
+        out[i] = sc_exp(lg - st.shift) / st.T;
     }
 }
 

@@ -603,7 +603,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                 const double nrm = er * ra;
                 const double x0 = -er_t * (al - g);
                 const double lp = (x0 + nrm) * kInvSqrt2, lm = (x0 - nrm) * kInvSqrt2;
-                const double A = exp(lp - sh), B = exp(lm - sh);
+                const double A = sc_exp(lp - sh), B = sc_exp(lm - sh);
                 cc = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
                 if (primary) {
                     T += A + B;
@@ -720,7 +720,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
         if (r < nr) {
             const double dW = v[0][0];
             const double lg = -er * (sg * dW - S);
-            e = exp(lg - sh);
+            e = sc_exp(lg - sh);
             if (primary) {
                 T += e;
                 M = fmax(M, lg);
@@ -926,6 +926,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     long long tcta = 0, tcta0 = 0;
     unsigned long long g_start = 0, g_end = 0;
 #endif
+    int64_t width_passes = 0;
     while (pp->action == kPass) {
         const PassParams ps = *pp;
 #ifdef SCMWU_PHASE_TIMING
@@ -935,6 +936,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         }
 #endif
         if (KIND == SC_SES) {
+            width_passes += (ps.check || ps.width) ? 1 : 0;
             if (ps.check) ses_pass<LPR, CPL, NB, FULL, 2>(p, m, ps, r0, r1, ws, pass_idx);
             else if (ps.width) ses_pass<LPR, CPL, NB, FULL, 1>(p, m, ps, r0, r1, ws, pass_idx);
             else ses_pass<LPR, CPL, NB, FULL, 0>(p, m, ps, r0, r1, ws, pass_idx);
@@ -1093,6 +1095,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         if (lane == 0) {
             if (!m.flags[1]) *p.status = ctl.status;
             p.res->passes = pass_idx;
+            p.res->width_passes = width_passes;
         }
     }
     __syncthreads();

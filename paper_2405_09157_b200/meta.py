@@ -91,6 +91,7 @@ class DeviceProblem:
         self.last_kernel_ms = 0.0
         self.total_kernel_ms = 0.0
         self.total_passes = 0
+        self.total_width_passes = 0
         self.calls = 0
 
     def progress(self, y_bar) -> float:
@@ -104,6 +105,7 @@ class DeviceProblem:
         self.last_kernel_ms = out.kernel_ms
         self.total_kernel_ms += out.kernel_ms
         self.total_passes += out.passes
+        self.total_width_passes += out.width_passes
         if out.counter_min is not None and (self.best_pd_dist is None
                                             or out.counter_min < self.best_pd_dist):
             self.handle.pd_commit(0)
@@ -212,6 +214,7 @@ class SolveReport:
     steps: list[SearchStep] = field(default_factory=list)
     kernel_ms: float = 0.0      # sum of persistent-kernel times (CUDA events)
     passes: int = 0             # streaming passes over the point matrix
+    width_passes: int = 0       # SES passes that evaluated the exact width residuals
 
 
 class WidthViolationError(RuntimeError):

@@ -153,6 +153,11 @@ void emu_set_exchange(sc_handle* h, emu_exchange_fn fn) {
     if (h) h->exchange = fn;
 }
 
+// the device passes' exponential, compiled for the host (tests/test_math.py)
+void emu_sc_exp(const double* x, double* out, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) out[i] = scmwu::sc_exp(x[i]);
+}
+
 int sc_create(const sc_problem* prob, const double* X, const double* X_tail,
               const double* radii, sc_handle** out) {
     if (!prob || !X || !out) return SC_EARG;
@@ -249,9 +254,10 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     const int rw = red_width(h->prob.kind, d);
     std::vector<double> red(rw), loc(rw);
     int act = c.begin(*args, h->red0.data(), y_tilde, best_y, &pp);
-    int64_t passes = 0;
+    int64_t passes = 0, width_passes = 0;
     while (act == kPass) {
         double* dst = h->prob.world > 1 ? loc.data() : red.data();
+        if (h->prob.kind == SC_SES && (pp.check || pp.width)) ++width_passes;
         if (h->prob.kind == SC_SES)
             pass_ses(h, pp, ysum.data(), yprev.data(), ywin.data(), dst);
         else
@@ -262,6 +268,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     }
     for (int j = 0; j < dd; ++j) best_y[j] = besty[j];
     res->passes = passes;
+    res->width_passes = width_passes;
     if (c.status == SC_EWIDTH) return fail(h, SC_EWIDTH, "width violation");
     return c.status;
 }

@@ -68,6 +68,11 @@ def main():
                       + " ".join(f"{i}:{int(sm[i])}" for i in order[-6:])
                       + "; fastest " + " ".join(f"{i}:{int(sm[i])}" for i in order[:4]),
                       flush=True)
+                h = G // 2
+                print("  mean cycles/pass first half %.0f second half %.0f; by decile: %s"
+                      % (per[:h].mean(), per[h:].mean(),
+                         " ".join("%.0f" % per[i * G // 10:(i + 1) * G // 10].mean()
+                                  for i in range(10))), flush=True)
             gs, ge = full[329:329 + G], full[489:489 + G]
             if gs.max() > 0:
                 base = gs.min()
