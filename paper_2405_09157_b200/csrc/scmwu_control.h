@@ -168,6 +168,8 @@ struct Control {
     int rung_index;
     double eta;
     int64_t win_head, win_count, win_len;  // ring indices (monotone) and live length
+    int64_t pos_head, pos_count;           // the same indices wrapped to the ring capacity
+                                           // (a 64-bit modulo per access cost ~100 cycles)
     // FTP early-stop state
     bool has_f_prev; double f_prev; int streak; bool early;
     bool has_f_start; double f_start;
@@ -186,6 +188,7 @@ struct Control {
     double dist_prev;        // SVM counter distance of iteration t (if check)
     bool check_prev;
     bool width_prev;         // SES: iteration t's width check needs the exact residuals
+    double inv_t_last;       // 1.0 / t, computed once per iteration
     // SVM pd bookkeeping
     bool has_counter_min; double counter_min;
     // latest iterate state (for p)
@@ -233,7 +236,7 @@ struct Control {
     SC_HD void offer_bar(double f) {
         if (!better(f)) return;
         has_best_f = true; best_f = f;
-        const double inv_t = 1.0 / (double)t;
+        const double inv_t = inv_t_last;   // == 1.0 / t (set by process_iterate)
 SC_UNROLL4
         for (int j = L::lane(); j < dd; j += L::nl()) v.besty[j] = v.ysum[j] * inv_t;
     }
@@ -356,7 +359,7 @@ SC_UNROLL4
     }
 
     SC_HD void reset_learner() {
-        t = 0; win_head = 0; win_count = 0; win_len = 0;
+        t = 0; win_head = 0; win_count = 0; win_len = 0; pos_head = 0; pos_count = 0;
         if (evict_idx >= 0) L::prefetch_wait();   // drop a pending prefetch of the old run
         evict_idx = -1;
         for (int j = L::lane(); j < dd; j += L::nl()) { v.ysum[j] = 0.0; v.wsum[j] = 0.0; }
@@ -469,7 +472,7 @@ SC_UNROLL4
             save_state(s.pd_pending, v.ysum, cur);
             if (pend_buf != nullptr) keep_state(pend_buf, v.ysum, cur);
         }
-        double* slot = s.ring + (win_count % s.ring_cap) * s.ring_stride;
+        double* slot = s.ring + pos_count * s.ring_stride;
         // SES width bound: with u_k = U_k / k the running average,
         //   |alpha - g_i| + |y_k - v_i| <= |alpha| + F(u_k) + |y_k - u_k|,
         //   F(u_k) <= F(u_{k-1}) + |u_k - u_{k-1}|,
@@ -477,7 +480,8 @@ SC_UNROLL4
         // produced this iterate.  When the bound is below the width rho the exact
         // residuals of y_k are not needed: the check cannot fail.
         const bool bound_ses = kind == SC_SES && k >= 2;
-        const double inv_k = 1.0 / (double)k, inv_km1 = bound_ses ? 1.0 / (double)(k - 1) : 0.0;
+        const double inv_k = 1.0 / (double)k, inv_km1 = bound_ses ? inv_t_last : 0.0;
+        inv_t_last = inv_k;
         double du2 = 0.0, dy2 = 0.0;
 SC_UNROLL4
         for (int j = ln; j < dd; j += nl) {
@@ -544,6 +548,7 @@ SC_UNROLL4
     SC_HD void push_window(int64_t tt) {
         const int nl = L::nl(), ln = L::lane();
         ++win_count; ++win_len;
+        if (++pos_count == s.ring_cap) pos_count = 0;
         const int64_t lim = kLadderBase > tt / 2 ? kLadderBase : tt / 2;
         while (win_len > lim) {
             if (evict_buf != nullptr && win_head == evict_idx) {
@@ -551,10 +556,11 @@ SC_UNROLL4
                 for (int j = ln; j < dd; j += nl) v.wsum[j] -= evict_buf[j];
                 evict_idx = -1;
             } else {
-                const double* old = s.ring + (win_head % s.ring_cap) * s.ring_stride;
+                const double* old = s.ring + pos_head * s.ring_stride;
                 for (int j = ln; j < dd; j += nl) v.wsum[j] -= L::ldcg(old + j);
             }
             ++win_head; --win_len;
+            if (++pos_head == s.ring_cap) pos_head = 0;
         }
     }
 
@@ -563,7 +569,7 @@ SC_UNROLL4
     SC_HD void prefetch_eviction() {
         if (evict_buf == nullptr || win_len < kLadderBase) return;
         evict_idx = win_head;
-        L::prefetch(evict_buf, s.ring + (win_head % s.ring_cap) * s.ring_stride, s.ring_stride);
+        L::prefetch(evict_buf, s.ring + pos_head * s.ring_stride, s.ring_stride);
     }
 
     SC_HD void write_pass(PassParams* pp) {

@@ -304,6 +304,7 @@ static int configure(sc_handle* h, int grid_req) {
     const bool two_sided = h->prob.kind == SC_SVM && n1 > 0 && n2 > 0;
     if (two_sided) G = std::max(G, 2);
     G = std::min(G, h->sms);
+    G = std::min(G, 160);   // the column fold loads at most 5 partials per lane
     if (G < 1) G = 1;
     if (two_sided && G < 2) { h->err = "SVM needs >= 2 SMs"; return SC_EARG; }
     // rows -> CTAs (SVM: P-CTAs then Q-CTAs, each CTA single-sided)

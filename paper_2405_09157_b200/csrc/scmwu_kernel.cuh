@@ -853,6 +853,9 @@ static __device__ __noinline__ void fold_all(const KParams& p, double* red, bool
 template <int KIND, int LPR, int CPL, int NB, bool FULL>
 __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constant__ KParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
+#ifdef SCMWU_PHASE_TIMING
+    __shared__ long long tt_sh[8];
+#endif
     const SmemMap m = carve(smem, p);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x;
@@ -888,7 +891,12 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         ctl.evict_buf = m.evict;
         ctl.pend_buf = m.pend;
 #ifdef SCMWU_PHASE_TIMING
-        if (p.timing != nullptr && b == 0 && lane == 0) ctl.tt = p.timing + 16 + 640;
+        // tail-section sums in shared memory (a global read-modify-write per mark cost
+        // ~1k cycles each and inflated the measured tail)
+        if (p.timing != nullptr && b == 0 && lane == 0) {
+            for (int i = 0; i < 8; ++i) tt_sh[i] = 0;
+            ctl.tt = tt_sh;
+        }
 #endif
         ctl.s = CtlSlots{p.ring, p.ring_cap, dd8, p.slots, p.slots + sl, p.slots + 2 * sl,
                          p.slots + 4 * sl};
@@ -1027,8 +1035,16 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             for (int j = c0 + warp; j < c1; j += kNW) {
                 const int op = red_op(KIND, j);
                 double acc = op_identity(op);
-                for (int q = lane; q < p.G; q += 32)
-                    acc = op_apply(op, acc, __ldcg(p.partials + (size_t)q * p.rw + j));
+                // all loads first (G <= 160: at most 5 per lane), then the fixed-order fold
+                double ld[5];
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const int q = lane + 32 * i;
+                    ld[i] = q < p.G ? __ldcg(p.partials + (size_t)q * p.rw + j) : 0.0;
+                }
+#pragma unroll
+                for (int i = 0; i < 5; ++i)
+                    if (lane + 32 * i < p.G) acc = op_apply(op, acc, ld[i]);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1)
                     acc = op_apply(op, acc, __shfl_xor_sync(0xffffffffu, acc, o));
@@ -1087,6 +1103,8 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         p.timing[16 + 320 + b] = (long long)g_start;   // last pass, global ns clock
         p.timing[16 + 480 + b] = (long long)g_end;
     }
+    if (p.timing != nullptr && b == 0 && tid == 0)
+        for (int i = 0; i < 8; ++i) p.timing[16 + 640 + i] = tt_sh[i];
 #endif
     // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
     stream_drain(p, m, warp, ws);

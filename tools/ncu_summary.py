@@ -44,6 +44,12 @@ def main():
             i = hdr.index(k)
             lines.append(f"| {k} | {vals[i]} | {units[i]} |")
             got[k] = (vals[i], units[i])
+    if passes is None and "--alg-bytes" in sys.argv and "dram__bytes_read.sum" in got:
+        # passes of the captured launch: each streams X once (read bytes / bytes of X)
+        alg = float(sys.argv[sys.argv.index("--alg-bytes") + 1])
+        v, u = got["dram__bytes_read.sum"]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
+        passes = max(1, round(float(v.replace(",", "")) * scale / alg))
     if passes and "dram__bytes_read.sum" in got:
         v, u = got["dram__bytes_read.sum"]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(u, 1)
@@ -53,6 +59,11 @@ def main():
         lines.append("")
         lines.append(f"DRAM traffic per streaming pass ({passes} passes in the launch): "
                      f"{tot / passes / 1e6:.1f} MB")
+        if "--traffic-json" in sys.argv:   # read by bench.py (roofline.traffic)
+            import json
+            with open(sys.argv[sys.argv.index("--traffic-json") + 1], "w") as fh:
+                json.dump({"dram_bytes_per_pass": tot / passes, "report": rep.split("/")[-1],
+                           "passes_in_launch": passes}, fh)
     # stall reasons
     stalls = []
     for i, h in enumerate(hdr):
