@@ -212,7 +212,7 @@ struct Control {
     long long tt_prev = 0;
     SC_HD void tmark(int i) {
 #if defined(__CUDA_ARCH__) && defined(SCMWU_PHASE_TIMING)
-        if (tt != nullptr) {
+        if (tt != nullptr && L::lane() == 0) {
             const long long now = clock64();
             if (i > 0) tt[i] += now - tt_prev;
             tt_prev = now;

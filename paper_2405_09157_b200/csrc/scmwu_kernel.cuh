@@ -320,6 +320,8 @@ struct SmemMap {
     double* wpart;     // kNW x pw
     PassParams* pp;
     sc_ftp_result* resd;
+    void* ctl;         // the control state between tails (warp 0 holds it in registers
+                       // only while the tail runs, so the passes get those registers)
     volatile int* flags;  // spare
     unsigned char* ring;
 };
@@ -334,6 +336,7 @@ __host__ __device__ inline size_t smem_fixed_bytes(int dd, int rw, int pw, int n
     b += (size_t)((rw + 1) & ~1) * 8;                  // red
     b += (size_t)kNW * ((pw + 1) & ~1) * 8;            // warp partials
     b += sizeof(PassParams) + sizeof(sc_ftp_result) + 16 * 4 + 64;
+    b += sizeof(Control<WarpLanes>) + 16;
     return (b + 127) & ~(size_t)127;
 }
 
@@ -362,6 +365,9 @@ __device__ inline SmemMap carve(unsigned char* base, const KParams& p) {
     off += sizeof(PassParams);
     m.resd = reinterpret_cast<sc_ftp_result*>(base + off);
     off += sizeof(sc_ftp_result);
+    off = (off + 15) & ~(size_t)15;
+    m.ctl = base + off;
+    off += sizeof(Control<WarpLanes>);
     m.flags = reinterpret_cast<volatile int*>(base + off);
     return m;
 }
@@ -560,8 +566,10 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
         const double* xs = reinterpret_cast<const double*>(st);
         const double* rs = reinterpret_cast<const double*>(st + p.rad_off) + (a & 1);
-        // phase A: per-lane partial sums of NB rows
+        // phase A: per-lane partial sums of NB rows; the differences stay in registers
+        // for phase C (one shared-memory read and one DFMA less per element)
         double v[NV][NB];
+        double dfk[NB][CPL];
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
             const int r = k * RPW + grp;
@@ -569,9 +577,11 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
             double sa = 0, sl = 0, sw = 0, sf = 0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
+                dfk[k][c] = 0.0;
                 if (ok[c]) {
                     const double x = xr[LPR * c];
                     const double df = fma(-t, x, U[c]);
+                    dfk[k][c] = df;
                     sa = fma(df, df, sa);
                     sl = fma(x, df, sl);
                     if (WIDTH) {
@@ -614,19 +624,13 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                 }
             }
         }
-        // phase C: S_d += c_i (U - t v_i), diff recomputed from the staged rows
+        // phase C: S_d += c_i (U - t v_i) from the differences kept in registers
+        // (zero in the unused column slots)
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
             const double ck = __shfl_sync(0xffffffffu, cc, grp * LPR + k * DUP);
-            const int rr = k * RPW + grp;
-            const double* xr = xs + (size_t)(rr < nr ? rr : 0) * ld + l;
 #pragma unroll
-            for (int c = 0; c < CPL; ++c) {
-                if (ok[c]) {
-                    const double df = fma(-t, xr[LPR * c], U[c]);
-                    Sd[c] = fma(ck, df, Sd[c]);
-                }
-            }
+            for (int c = 0; c < CPL; ++c) Sd[c] = fma(ck, dfk[k][c], Sd[c]);
         }
         release_stage(p, m, r0, r1, warp, ws);
     }
@@ -693,6 +697,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
         const double* xs = reinterpret_cast<const double*>(st);
         double v[NV][NB];
+        double xk[NB][CPL];   // the staged rows, kept in registers for the G update
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
             const int r = k * RPW + grp;
@@ -700,8 +705,10 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
             double dW = 0, dw = 0, dy = 0, dz = 0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
+                xk[k][c] = 0.0;
                 if (ok[c]) {
                     const double x = xr[LPR * c];
+                    xk[k][c] = x;
                     dW = fma(x, W[c], dW);
                     dw = fma(x, wq[c], dw);
                     if (CHECK) {
@@ -739,11 +746,8 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
             const double ek = __shfl_sync(0xffffffffu, e, grp * LPR + k * DUP);
-            const int rr = k * RPW + grp;
-            const double* xr = xs + (size_t)(rr < nr ? rr : 0) * ld + l;
 #pragma unroll
-            for (int c = 0; c < CPL; ++c)
-                if (ok[c]) G[c] = fma(ek, xr[LPR * c], G[c]);
+            for (int c = 0; c < CPL; ++c) G[c] = fma(ek, xk[k][c], G[c]);
         }
         release_stage(p, m, r0, r1, warp, ws);
     }
@@ -875,10 +879,15 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     // ------------------------------------------------------------ consumers
     const int dd8 = dd8_of(p.dd);
     const int tid = threadIdx.x;
-    Control<WarpLanes> ctl;
+    // The control state lives in shared memory between tails: warp 0 loads it into
+    // registers for the tail and stores it back, so it is dead (no registers) during the
+    // streaming passes.  Every lane holds identical scalars; lane 0 stores them.
+    using Ctl = Control<WarpLanes>;
+    Ctl* const ctl_sm = reinterpret_cast<Ctl*>(m.ctl);
     PassParams* pp = m.pp;
     double* y_tilde = b == 0 ? p.y_tilde : m.ytd;
     if (warp == 0) {
+        Ctl ctl;
         ctl.kind = KIND; ctl.d = p.d; ctl.dd = p.dd; ctl.is_max = KIND == SC_SES;
         ctl.rho = p.rho; ctl.inv_rho = p.inv_rho; ctl.R = p.R; ctl.ln_r = p.ln_r;
         ctl.D = p.D; ctl.g1 = p.g1;
@@ -906,7 +915,10 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         }
         __syncwarp();
         int act = ctl.begin(p.args, p.red0, y_tilde, nullptr, pp);
-        if (lane == 0) pp->action = act;
+        if (lane == 0) {
+            pp->action = act;
+            *ctl_sm = ctl;
+        }
     }
     consumer_sync();
 
@@ -1081,8 +1093,13 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             break;
         }
         if (warp == 0) {
+            Ctl ctl = *ctl_sm;
             int act = ctl.after_pass(m.red, p.red0, y_tilde, pp);
-            if (lane == 0) pp->action = act;
+            __syncwarp();
+            if (lane == 0) {
+                pp->action = act;
+                *ctl_sm = ctl;
+            }
             stream_flush(p, m, r0, r1, warp, ws);
         }
         SCMWU_TMARK(7)
@@ -1109,9 +1126,10 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
     stream_drain(p, m, warp, ws);
     if (b == 0 && warp == 0) {
-        for (int j = lane; j < p.dd; j += 32) p.best_y[j] = ctl.v.besty[j];
+        __syncwarp();
+        for (int j = lane; j < p.dd; j += 32) p.best_y[j] = ctl_sm->v.besty[j];
         if (lane == 0) {
-            if (!m.flags[1]) *p.status = ctl.status;
+            if (!m.flags[1]) *p.status = ctl_sm->status;
             p.res->passes = pass_idx;
             p.res->width_passes = width_passes;
         }
