@@ -168,8 +168,9 @@ int64_t sc_launches(const sc_handle* h);
  * out[0..9) per-phase SM-cycle sums of the last sc_ftp as seen by CTA 0 (pass, warp
  * join, CTA partial, barrier 1, fold, barrier 2, reduced read, control tail, tail join),
  * out[9..169) each CTA's streaming cycles, out[169..329) its SM id, out[329..489) and
- * out[489..649) global-timer ns at the start / end of its last pass, out[649..656)
- * cycle sums of the control tail's sections (CTA 0); zeros otherwise. */
+ * out[489..649) global-timer ns at the start / end of its last pass, out[649..809) and
+ * out[809..969) at its arrival at / release from that pass's first grid barrier,
+ * out[969..976) cycle sums of the control tail's sections (CTA 0); zeros otherwise. */
 int sc_debug_timing(sc_handle* h, double* out);
 int sc_pd_pair(sc_handle* h, double* mu /* n1 */, double* gam /* n - n1 */, double* dist);
 /* Row sharding (world > 1).  The per-pass exchange runs INSIDE the persistent kernel:

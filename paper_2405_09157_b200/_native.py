@@ -327,8 +327,9 @@ class Handle:
     def debug_timing(self) -> np.ndarray:
         """[0:9] phase cycles of CTA 0, [9:169] per-CTA streaming cycles, [169:329] SM ids,
         [329:489] / [489:649] global-ns start / end of each CTA's last streaming pass,
-        [649:656] cycle sums of the control tail's sections (CTA 0)."""
-        out = np.zeros(9 + 4 * 160 + 7)
+        [649:809] / [809:969] global-ns arrival at / release from its first grid barrier,
+        [969:976] cycle sums of the control tail's sections (CTA 0)."""
+        out = np.zeros(9 + 6 * 160 + 7)
         self._check(self.engine.lib.sc_debug_timing(self.h, _ptr(out)), "sc_debug_timing")
         return out
 

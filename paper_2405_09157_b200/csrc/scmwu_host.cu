@@ -2,6 +2,10 @@
 // launch configuration and the one-off kernels (progress, iterate, column sums).
 #include <stdlib.h>
 
+#include <cmath>
+#include <map>
+#include <mutex>
+
 #include "scmwu_kernel.cuh"
 
 namespace scmwu {
@@ -194,6 +198,58 @@ __global__ void gen_kernel(double* X, int ld, int d, int64_t rows, int64_t grow0
     if (dmax && lane == 0 && best > 0.0) atomicMax(dmax, (unsigned long long)__double_as_longlong(best));
 }
 
+// -------------------------------------------------------------------------------------
+// Per-SM streaming-rate calibration (one CTA per SM, all SMs streaming at once): every
+// CTA pulls its own `per` bytes through per-warp bulk-copy rings, the persistent kernel's
+// pattern, and records its cycles and SM id.  On B200 the rates differ by SM position
+// (measured: the first TPC of every 16-SM group ~25% faster than the rest, the others
+// within ~10% of each other; tools/die_probe.cu, profiles/r01_overhead.md).
+__global__ void __launch_bounds__(256, 1) calib_kernel(const char* X, size_t per, int tile,
+                                                       int S, long long* cyc, int* smid) {
+    extern __shared__ __align__(128) unsigned char csm[];
+    constexpr int W = 8;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(csm);
+    unsigned char* ring = csm + 1024;
+    const char* base = X + (size_t)blockIdx.x * per;
+    const int ntiles = (int)(per / tile);
+    if (lane == 0)
+        for (int s = 0; s < S; ++s) mbar_init(&bars[w * S + s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const long long t0 = clock64();
+    const int mine = (ntiles - w + W - 1) / W;
+    auto issue = [&](int q, int st) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(&bars[w * S + st], (uint32_t)tile);
+        bulk_g2s(ring + (size_t)(w * S + st) * tile, base + (size_t)(w + q * W) * tile,
+                 (uint32_t)tile, &bars[w * S + st]);
+    };
+    if (lane == 0)
+        for (int q = 0; q < S && q < mine; ++q) issue(q, q);
+    int issued = min(S, mine), s_issue = issued % S, s = 0;
+    uint32_t phase = 0;
+    double acc = 0.0;
+    for (int q = 0; q < mine; ++q) {
+        mbar_wait(&bars[w * S + s], phase);
+        acc += reinterpret_cast<const double*>(ring + (size_t)(w * S + s) * tile)[lane];
+        __syncwarp();
+        if (issued < mine) {
+            if (lane == 0) issue(issued, s_issue);
+            ++issued;
+            s_issue = s_issue + 1 == S ? 0 : s_issue + 1;
+        }
+        if (++s == S) { s = 0; phase ^= 1u; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cyc[blockIdx.x] = clock64() - t0 + (acc == 1.2345 ? 1 : 0);
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        smid[blockIdx.x] = (int)sm;
+    }
+}
+
 
 }  // namespace scmwu
 
@@ -279,6 +335,7 @@ struct sc_handle {
     // host state
     std::vector<double> red0_h;
     bool has_sep = false, has_callmin = false;
+    bool by_smid = false;            // rows balanced per SM (configure)
     std::string err;
 };
 
@@ -291,6 +348,87 @@ static int cuda_fail(sc_handle* h, cudaError_t e, const char* what) {
         cudaError_t _e = (call);                         \
         if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
     } while (0)
+
+// Per-device SM weights from calib_kernel, measured once per process and shared by every
+// handle on that device (so two handles of the same instance partition rows identically
+// and give bit-identical results).  Weights are the streaming rates quantised to 1/64 of
+// the fastest SM, which keeps the partition stable against timing noise.  Empty: no
+// balancing (SCMWU_BALANCE=0, SM ids not 0..#SMs-1, or the probe could not run).
+static std::mutex g_calib_mu;
+static std::map<int, std::vector<double>> g_calib;
+
+static const std::vector<double>& sm_weights(sc_handle* h) {
+    std::lock_guard<std::mutex> lock(g_calib_mu);
+    const int dev = h->prob.device;
+    auto it = g_calib.find(dev);
+    if (it != g_calib.end()) return it->second;
+    std::vector<double>& w = g_calib[dev];
+    // opt-in (SCMWU_BALANCE=1): the probe's pure-streaming rates overshoot for the compute
+    // loaded passes (SES C2 136 -> 149 us/pass, SVM C3 137 -> 135.5, same box), so the
+    // default keeps the equal cyclic partition
+    const char* e = getenv("SCMWU_BALANCE");
+    if (e == nullptr || atoi(e) == 0) return w;
+    const int G = h->sms, S = 2, tile = 13312;
+    const size_t per = (size_t)tile * 8 * 48;          // 48 tiles per warp (~5 MB per SM)
+    char* buf = nullptr;
+    long long* cyc = nullptr;
+    int* sid = nullptr;
+    if (cudaMalloc(&buf, per * G) != cudaSuccess) { cudaGetLastError(); return w; }
+    bool ok = cudaMalloc(&cyc, G * sizeof(long long)) == cudaSuccess &&
+              cudaMalloc(&sid, G * sizeof(int)) == cudaSuccess &&
+              cudaMemsetAsync(buf, 0, per * G, h->stream) == cudaSuccess;
+    const int smem = 1024 + 8 * S * tile;
+    ok = ok && cudaFuncSetAttribute(calib_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem) == cudaSuccess;
+    std::vector<long long> best(G, 0);
+    std::vector<long long> hc(G);
+    std::vector<int> hs(G);
+    for (int rep = 0; ok && rep < 4; ++rep) {
+        calib_kernel<<<G, 256, smem, h->stream>>>(buf, per, tile, S, cyc, sid);
+        ok = cudaStreamSynchronize(h->stream) == cudaSuccess &&
+             cudaMemcpy(hc.data(), cyc, G * sizeof(long long), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess &&
+             cudaMemcpy(hs.data(), sid, G * sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
+        if (!ok || rep == 0) continue;                   // rep 0 warms up
+        for (int b = 0; b < G; ++b) {
+            if (hs[b] < 0 || hs[b] >= G) { ok = false; break; }
+            long long& m = best[hs[b]];
+            m = m == 0 ? hc[b] : std::min(m, hc[b]);
+        }
+    }
+    h->launches += 4;
+    if (buf) cudaFree(buf);
+    if (cyc) cudaFree(cyc);
+    if (sid) cudaFree(sid);
+    cudaGetLastError();
+    for (int s = 0; ok && s < G; ++s) ok = best[s] > 0;   // every SM id seen
+    if (!ok) return w;
+    const long long fastest = *std::min_element(best.begin(), best.end());
+    w.resize(G);
+    for (int s = 0; s < G; ++s)
+        w[s] = std::max(1.0, std::round(64.0 * (double)fastest / (double)best[s])) / 64.0;
+    return w;
+}
+
+// tiles [0, T) of one side split over `slots` contiguous blocks in proportion to the
+// weights (largest remainder, ties to the lower slot)
+static std::vector<int64_t> weighted_split(int64_t T, const std::vector<double>& w) {
+    const int k = (int)w.size();
+    double W = 0.0;
+    for (double x : w) W += x;
+    std::vector<int64_t> cnt(k);
+    std::vector<std::pair<double, int>> rem(k);
+    int64_t used = 0;
+    for (int i = 0; i < k; ++i) {
+        const double ideal = (double)T * w[i] / W;
+        cnt[i] = (int64_t)std::floor(ideal);
+        used += cnt[i];
+        rem[i] = {-(ideal - (double)cnt[i]), i};
+    }
+    std::sort(rem.begin(), rem.end());
+    for (int64_t r = 0; r < T - used; ++r) ++cnt[rem[(size_t)(r % k)].second];
+    return cnt;
+}
 
 static int configure(sc_handle* h, int grid_req) {
     const int d = h->prob.d;
@@ -328,9 +466,61 @@ static int configure(sc_handle* h, int grid_req) {
     h->rad_off = (xb + 15) & ~15u;
     const uint32_t radb = h->prob.kind == SC_SES ? (uint32_t)((tr + 2) * 8) : 0u;
     h->stage_stride = (h->rad_off + radb + 127) & ~127u;
-    int64_t max_rows = 0;
-    for (int b = 0; b < G; ++b) max_rows = std::max(max_rows, rb[b + 1] - rb[b]);
-    const int nwt = (int)((max_rows + tr - 1) / tr);
+    // per-CTA tile sequence {first row, end row, row stride between its warp tiles}.
+    // Cyclic (default): CTA c of a side with g CTAs takes that side's tiles c, c+g, ...,
+    // so every CTA streams from the whole address range (per-CTA pass times were 13-18%
+    // apart with contiguous blocks on some boxes, growing with the block's address,
+    // profiles/r01_overhead.md).  SCMWU_CONTIG=1: contiguous blocks.
+    const bool cyclic = getenv("SCMWU_CONTIG") == nullptr;
+    std::vector<int64_t> cta(3 * (size_t)G);
+    // one CTA per SM: contiguous tile blocks per SM id sized by the SM's measured rate
+    h->by_smid = false;
+    if (G == h->sms) {
+        const std::vector<double>& w = sm_weights(h);
+        if ((int)w.size() == G) {
+            h->by_smid = true;
+            auto fill = [&](int s0, int s1, int64_t rs, int64_t re) {
+                const int64_t T = (re - rs + tr - 1) / tr;
+                const std::vector<int64_t> cnt =
+                    weighted_split(T, std::vector<double>(w.begin() + s0, w.begin() + s1));
+                int64_t t0 = 0;
+                for (int i = 0; i < s1 - s0; ++i) {
+                    const int s = s0 + i;
+                    cta[3 * s] = rs + t0 * tr;
+                    cta[3 * s + 1] = std::min(re, rs + (t0 + cnt[i]) * tr);
+                    cta[3 * s + 2] = tr;
+                    t0 += cnt[i];
+                }
+            };
+            if (two_sided) {
+                fill(0, h->gP, 0, n1);
+                fill(h->gP, G, n1, n);
+            } else {
+                fill(0, G, 0, n);
+            }
+        }
+    }
+    int nwt = 0;
+    for (int b = 0; b < G; ++b) {
+        int64_t c0, c1, st;
+        if (h->by_smid) {
+            c0 = cta[3 * b]; c1 = cta[3 * b + 1]; st = cta[3 * b + 2];
+        } else if (!cyclic) {
+            c0 = rb[b]; c1 = rb[b + 1]; st = tr;
+        } else {
+            int64_t s0 = 0, s1 = n;
+            int gc = G, ci = b;
+            if (two_sided) {
+                const bool P = b < h->gP;
+                s0 = P ? 0 : n1; s1 = P ? n1 : n;
+                gc = P ? h->gP : G - h->gP; ci = P ? b : b - h->gP;
+            }
+            c0 = s0 + (int64_t)ci * tr; c1 = s1; st = (int64_t)gc * tr;
+        }
+        cta[3 * b] = c0; cta[3 * b + 1] = c1; cta[3 * b + 2] = st;
+        const int t = c1 > c0 ? (int)((c1 - c0 + st - 1) / st) : 0;
+        nwt = std::max(nwt, t);
+    }
     const int per_warp = (nwt + kNW - 1) / kNW;
     auto need = [&](int sw) {
         return (size_t)kNW * sw * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, kNW * sw);
@@ -347,8 +537,8 @@ static int configure(sc_handle* h, int grid_req) {
     h->grid = G;
     if (h->row_begin) cudaFree(h->row_begin);
     if (h->partials) cudaFree(h->partials);
-    CK(cudaMalloc(&h->row_begin, (G + 1) * sizeof(int64_t)), "alloc rows");
-    CK(cudaMemcpy(h->row_begin, rb.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice),
+    CK(cudaMalloc(&h->row_begin, cta.size() * sizeof(int64_t)), "alloc rows");
+    CK(cudaMemcpy(h->row_begin, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
        "copy rows");
     CK(cudaMalloc(&h->partials, (size_t)G * h->rw * sizeof(double)), "alloc partials");
     CK(cudaFuncSetAttribute(h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem),
@@ -665,6 +855,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     // (SCMWU_DEFER_PREFETCH + SCMWU_FLUSH_AFTER_TAIL)
     p.wrap_prefetch = getenv("SCMWU_DEFER_PREFETCH") ? 0 : 1;
     p.flush_after_tail = getenv("SCMWU_FLUSH_AFTER_TAIL") ? 1 : 0;
+    p.by_smid = h->by_smid ? 1 : 0;
     p.X = h->X; p.radii = h->radii; p.row_begin = h->row_begin;
     p.rho = h->prob.rho; p.inv_rho = 1.0 / h->prob.rho; p.R = h->prob.R; p.ln_r = h->prob.ln_r;
     p.D = h->prob.D; p.g1 = h->g1;
@@ -674,9 +865,9 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     p.args = *args; p.res = h->res; p.y_tilde = h->y_tilde; p.best_y = h->best_y;
     p.status = h->status; p.stage_stride = h->stage_stride; p.rad_off = h->rad_off;
     if (!h->timing && getenv("SCMWU_TIMING")) {
-        CK(cudaMalloc(&h->timing, (16 + 4 * 160 + 16) * 8), "alloc timing");
+        CK(cudaMalloc(&h->timing, (16 + 6 * 160 + 16) * 8), "alloc timing");
     }
-    if (h->timing) CK(cudaMemsetAsync(h->timing, 0, (16 + 4 * 160 + 16) * 8, h->stream), "timing");
+    if (h->timing) CK(cudaMemsetAsync(h->timing, 0, (16 + 6 * 160 + 16) * 8, h->stream), "timing");
     p.timing = h->timing;
     p.v1 = h->v1;
     p.world = h->prob.world;
@@ -921,12 +1112,12 @@ int64_t sc_launches(const sc_handle* h) { return h ? h->launches : 0; }
 
 int sc_debug_timing(sc_handle* h, double* out) {
     if (!h || !out) return SC_EARG;
-    if (!h->timing) { for (int i = 0; i < 9 + 4 * 160 + 7; ++i) out[i] = 0.0; return SC_OK; }
-    long long t[16 + 4 * 160 + 16];
+    if (!h->timing) { for (int i = 0; i < 9 + 6 * 160 + 7; ++i) out[i] = 0.0; return SC_OK; }
+    long long t[16 + 6 * 160 + 16];
     CK(cudaMemcpy(t, h->timing, sizeof(t), cudaMemcpyDeviceToHost), "copy timing");
     for (int i = 0; i < 9; ++i) out[i] = (double)t[i];
-    for (int i = 0; i < 4 * 160; ++i) out[9 + i] = (double)t[16 + i];
-    for (int i = 0; i < 7; ++i) out[9 + 4 * 160 + i] = (double)t[16 + 4 * 160 + i];
+    for (int i = 0; i < 6 * 160; ++i) out[9 + i] = (double)t[16 + i];
+    for (int i = 0; i < 7; ++i) out[9 + 6 * 160 + i] = (double)t[16 + 6 * 160 + i];
     return SC_OK;
 }
 

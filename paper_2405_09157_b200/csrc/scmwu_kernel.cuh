@@ -134,10 +134,11 @@ struct KParams {
     int fold_mode;                     // kFoldTwoBarriers / kFoldRedundant / kFoldLast
     int wrap_prefetch;                 // 1: prefetch the next pass during the reduction
     int flush_after_tail;              // 1: issue the next pass's copies after the tail
+    int by_smid;                       // 1: work slot = SM id (G == #SMs, balanced rows)
     int64_t n, n1;
     const double* X;           // n x ld (ld even, padded with zeros)
     const double* radii;       // SES: n rounded up to even (zero padded)
-    const int64_t* row_begin;  // G + 1
+    const int64_t* row_begin;  // per CTA {first row, end row, row stride of its warp tiles}
     double rho, inv_rho, R, ln_r, D, g1;
     const double* red0;        // reduced vector of iterate 1 (all logits 0)
     double* partials;          // G x rw
@@ -391,12 +392,14 @@ struct WarpStream {
     uint32_t phase;   // parity of that stage's full barrier
     int s_issue;      // stage the next copy goes to (tiles fill stages cyclically)
     int inflight;     // issued and not yet consumed
+    int64_t tstride;  // rows between this CTA's consecutive warp tiles
 };
 
 __device__ __forceinline__ void issue_tile(const KParams& p, const SmemMap& m, int64_t r0,
-                                           int64_t r1, int w, int q, int stage) {
+                                           int64_t r1, int64_t tstride, int w, int q,
+                                           int stage) {
     const int slot = w * p.stages + stage;
-    const int64_t a = r0 + (int64_t)(w + q * kNW) * p.tile_rows;
+    const int64_t a = r0 + (int64_t)(w + q * kNW) * tstride;
     const int64_t b = min(r1, a + (int64_t)p.tile_rows);
     unsigned char* dst = m.ring + (size_t)slot * p.stage_stride;
     const uint32_t xb = (uint32_t)((b - a) * p.ld * 8);
@@ -421,7 +424,7 @@ __device__ __forceinline__ void stream_start(const KParams& p, const SmemMap& m,
     ws.phase = 0;
     const int first = ws.cnt < p.stages ? ws.cnt : p.stages;
     if ((threadIdx.x & 31) == 0)
-        for (int q = 0; q < first; ++q) issue_tile(p, m, r0, r1, w, q, q);
+        for (int q = 0; q < first; ++q) issue_tile(p, m, r0, r1, ws.tstride, w,q, q);
     ws.issued = first;
     ws.deferred = 0;
     ws.inflight = first;
@@ -442,7 +445,7 @@ __device__ __forceinline__ void stream_flush(const KParams& p, const SmemMap& m,
     }
     if ((threadIdx.x & 31) == 0)
         for (int q = 0; q < ws.deferred; ++q) {
-            issue_tile(p, m, r0, r1, w, q, ws.s_issue);
+            issue_tile(p, m, r0, r1, ws.tstride, w,q, ws.s_issue);
             ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
         }
     else
@@ -471,12 +474,12 @@ __device__ __forceinline__ void release_stage(const KParams& p, const SmemMap& m
     __syncwarp();
     --ws.inflight;
     if (ws.issued < ws.cnt) {            // the next tile of this pass
-        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, w, ws.issued, ws.s_issue);
+        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, ws.tstride, w,ws.issued, ws.s_issue);
         ++ws.issued;
         ++ws.inflight;
         ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
     } else if (p.wrap_prefetch) {        // (A/B) prefetch the next pass right away
-        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, w, ws.deferred, ws.s_issue);
+        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, ws.tstride, w,ws.deferred, ws.s_issue);
         ++ws.deferred;
         ++ws.inflight;
         ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
@@ -562,7 +565,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
     for (int q = 0; q < ws.cnt; ++q) {
         const int j = warp + q * kNW;
         const unsigned char* st = acquire_stage(p, m, warp, ws, pass_idx);
-        const int64_t a = r0 + (int64_t)j * p.tile_rows;
+        const int64_t a = r0 + (int64_t)j * ws.tstride;
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
         const double* xs = reinterpret_cast<const double*>(st);
         const double* rs = reinterpret_cast<const double*>(st + p.rad_off) + (a & 1);
@@ -693,7 +696,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
     for (int q = 0; q < ws.cnt; ++q) {
         const int j = warp + q * kNW;
         const unsigned char* st = acquire_stage(p, m, warp, ws, pass_idx);
-        const int64_t a = r0 + (int64_t)j * p.tile_rows;
+        const int64_t a = r0 + (int64_t)j * ws.tstride;
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
         const double* xs = reinterpret_cast<const double*>(st);
         double v[NV][NB];
@@ -863,9 +866,20 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     const SmemMap m = carve(smem, p);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x;
-    const int64_t r0 = p.row_begin[b], r1 = p.row_begin[b + 1];
-    const int nwt = (int)((r1 - r0 + p.tile_rows - 1) / p.tile_rows);
-    const bool isP = KIND == SC_SVM && b < p.gP;
+    // work slot: the CTA index, or (one CTA per SM, rows balanced by the measured
+    // per-SM streaming rates) the SM id, so a slot's rows and its place in the fixed-order
+    // fold do not depend on how this launch mapped CTAs to SMs
+    int slot = b;
+    if (p.by_smid) {
+        unsigned s;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+        slot = (int)s;
+    }
+    // this slot's warp tiles: tile j covers rows [r0 + j * tstride, + tile_rows) below r1
+    const int64_t r0 = p.row_begin[3 * slot], r1 = p.row_begin[3 * slot + 1];
+    const int64_t tstride = p.row_begin[3 * slot + 2];
+    const int nwt = r1 > r0 ? (int)((r1 - r0 + tstride - 1) / tstride) : 0;
+    const bool isP = KIND == SC_SVM && slot < p.gP;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNW * p.stages; ++s) mbar_init(&m.full[s], 1);
         m.flags[0] = 0;
@@ -874,6 +888,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     }
     __syncthreads();
     WarpStream ws;
+    ws.tstride = tstride;
     stream_start(p, m, r0, r1, warp, ws, nwt);
 
     // ------------------------------------------------------------ consumers
@@ -944,7 +959,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     }
 #ifdef SCMWU_PHASE_TIMING
     long long tcta = 0, tcta0 = 0;
-    unsigned long long g_start = 0, g_end = 0;
+    unsigned long long g_start = 0, g_end = 0, g_arr = 0, g_rel = 0;
 #endif
     int64_t width_passes = 0;
     while (pp->action == kPass) {
@@ -997,7 +1012,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
                     v = acc;
                 }
             }
-            p.partials[(size_t)b * p.rw + j] = v;
+            p.partials[(size_t)slot * p.rw + j] = v;
         }
         SCMWU_TMARK(2)
         if (kFoldVariants && p.fold_mode == kFoldLast) {
@@ -1041,7 +1056,14 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             consumer_sync();
             SCMWU_TMARK(6)
         } else {
+#ifdef SCMWU_PHASE_TIMING
+            consumer_sync();
+            if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_arr));
+#endif
             grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
+#ifdef SCMWU_PHASE_TIMING
+            if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_rel));
+#endif
             SCMWU_TMARK(3)
             // column-distributed fold over the G partials: warp per column, fixed tree
             for (int j = c0 + warp; j < c1; j += kNW) {
@@ -1119,9 +1141,11 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         p.timing[16 + 160 + b] = smid;
         p.timing[16 + 320 + b] = (long long)g_start;   // last pass, global ns clock
         p.timing[16 + 480 + b] = (long long)g_end;
+        p.timing[16 + 640 + b] = (long long)g_arr;     // last pass: first grid barrier
+        p.timing[16 + 800 + b] = (long long)g_rel;
     }
     if (p.timing != nullptr && b == 0 && tid == 0)
-        for (int i = 0; i < 8; ++i) p.timing[16 + 640 + i] = tt_sh[i];
+        for (int i = 0; i < 8; ++i) p.timing[16 + 960 + i] = tt_sh[i];
 #endif
     // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
     stream_drain(p, m, warp, ws);

@@ -416,7 +416,7 @@ int sc_elapsed(sc_handle* h, float* ms) {
 int64_t sc_launches(const sc_handle* h) { (void)h; return 0; }
 int sc_debug_timing(sc_handle* h, double* out) {
     if (!h || !out) return SC_EARG;
-    for (int i = 0; i < 9 + 4 * 160 + 7; ++i) out[i] = 0.0;
+    for (int i = 0; i < 9 + 6 * 160 + 7; ++i) out[i] = 0.0;
     return SC_OK;
 }
 

@@ -80,7 +80,15 @@ def main():
                       f"spread {ge.max() - ge.min():.0f}, CTA0 start +{gs[0] - base:.0f} end "
                       f"+{ge[0] - base:.0f}, latest start CTA {int(np.argmax(gs))}, latest end "
                       f"CTA {int(np.argmax(ge))} (+{ge.max() - base:.0f})", flush=True)
-            ts = full[649:656] / max(r.passes, 1)
+            ga, gr = full[649:649 + G], full[809:809 + G]
+            if ga.max() > 0:
+                la = ga.max()
+                print(f"  last pass, first barrier: arrival spread {ga.max() - ga.min():.0f} ns, "
+                      f"CTA0 arrives {la - ga[0]:.0f} ns before the last; release after the "
+                      f"last arrival: min {(gr - la).min():.0f} median {np.median(gr - la):.0f} "
+                      f"max {(gr - la).max():.0f} ns; last arriver CTA {int(np.argmax(ga))}",
+                      flush=True)
+            ts = full[969:976] / max(r.passes, 1)
             if ts.sum() > 0:
                 print("  tail sections cycles/pass: finish_iteration %.0f, oracle epilogue %.0f,"
                       " update loops %.0f, window %.0f, checks+shift %.0f, write_pass %.0f"
