@@ -5,6 +5,6 @@ bash tools/profile_round.sh r01c ses_c2 --steps 3 --warmup 3 > gpurun_out/round_
 python bench.py --workload svm_c3 --steps 1 --warmup 3 > gpurun_out/bench_r01c_svm_c3.json 2> gpurun_out/bench_r01c_svm_c3.err
 python bench.py --workload svm_c5_gen --steps 3 --warmup 3 > gpurun_out/bench_r01c_svm_c5_gen.json 2> gpurun_out/bench_r01c_svm_c5_gen.err
 python bench.py --workload ses_c4_gen --steps 1 --warmup 3 > gpurun_out/bench_r01c_ses_c4_gen.json 2> gpurun_out/bench_r01c_ses_c4_gen.err
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:scmwu_kernel -s 2 -c 1 -o gpurun_out/full_r01c_svm_c3 python tools/gen_perf.py svm 500000 100 --horizon 64 --reps 1 > /dev/null 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:scmwu_kernel -s 2 -c 1 -o gpurun_out/full_r01c_svm_c5 python tools/gen_perf.py svm 1000000 512 --horizon 16 --reps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:scmwu_kernel -s 1 -c 1 -o gpurun_out/full_r01c_svm_c3 python tools/gen_perf.py svm 500000 100 --horizon 64 --reps 1 > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:scmwu_kernel -s 1 -c 1 -o gpurun_out/full_r01c_svm_c5 python tools/gen_perf.py svm 1000000 512 --horizon 16 --reps 1 > /dev/null 2>&1
 ls -la gpurun_out | grep r01c
