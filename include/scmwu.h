@@ -151,6 +151,17 @@ int sc_create_generated(sc_problem* prob, const sc_gen* gen, double* v1_out,
 int sc_set_range(sc_handle* h, double D);
 /* Copy `count` resident rows starting at local row `first` to out (count x d, row-major). */
 int sc_read_rows(sc_handle* h, int64_t first, int64_t count, double* out);
+/* Independent verification baselines over a resident single-GPU instance (SURVEY §8(f)
+ * row 3), one cooperative launch each:
+ *   sc_meb_baseline      Badoiu-Clarkson walk of R/baselines.py:34-85 (meb_baseline) for
+ *                        `iters` = ceil(1/eps_base^2) steps on an SES handle; center (d) and
+ *                        the covering radius max_i |v_i - c| + r_i (value, may be NULL).
+ *   sc_gilbert_baseline  Frank-Wolfe / Gilbert of R/baselines.py:88-161 on an SVM handle:
+ *                        |z| (value), the last linearisation gap, the iteration count and,
+ *                        if not NULL, the weights mu (n1) / gam (n - n1). */
+int sc_meb_baseline(sc_handle* h, int64_t iters, double* center, double* value);
+int sc_gilbert_baseline(sc_handle* h, double gap_tol, int64_t max_iters, double* value,
+                        double* gap, int64_t* iterations, double* mu, double* gam);
 int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
            double* y_tilde /* dual_dim */, double* best_y /* dual_dim */);
 int sc_progress(sc_handle* h, const double* y /* d values */, double* f);

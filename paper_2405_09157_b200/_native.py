@@ -81,7 +81,7 @@ EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "
            "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_debug_timing",
            "sc_local_red0", "sc_progress_parts", "sc_set_globals", "sc_ipc_handle",
            "sc_connect", "sc_last_error", "sc_destroy", "sc_version", "sc_create_generated",
-           "sc_set_range", "sc_read_rows")
+           "sc_set_range", "sc_read_rows", "sc_meb_baseline", "sc_gilbert_baseline")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -131,6 +131,9 @@ class Engine:
                                             _dp, ctypes.POINTER(vp)]
         lib.sc_set_range.argtypes = [vp, ctypes.c_double]
         lib.sc_read_rows.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, _dp]
+        lib.sc_meb_baseline.argtypes = [vp, ctypes.c_int64, _dp, _dp]
+        lib.sc_gilbert_baseline.argtypes = [vp, ctypes.c_double, ctypes.c_int64, _dp, _dp,
+                                            ctypes.POINTER(ctypes.c_int64), _dp, _dp]
         self.lib = lib
 
     def create_generated(self, kind: int, n: int, d: int, seed: int, dist: int,
@@ -288,6 +291,24 @@ class Handle:
     def set_range(self, D: float) -> None:
         self._check(self.engine.lib.sc_set_range(self.h, D), "sc_set_range")
         self.prob.D = D
+
+    def meb_baseline(self, iters: int) -> tuple[np.ndarray, float]:
+        c = np.zeros(self.d)
+        v = ctypes.c_double()
+        self._check(self.engine.lib.sc_meb_baseline(self.h, iters, _ptr(c), ctypes.byref(v)),
+                    "sc_meb_baseline")
+        return c, float(v.value)
+
+    def gilbert_baseline(self, gap_tol: float, max_iters: int, weights: bool = True):
+        n1 = self.prob.n1_local
+        n2 = self.prob.n_local - n1
+        mu = np.zeros(n1) if weights else None
+        gam = np.zeros(n2) if weights else None
+        v, g, it = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        self._check(self.engine.lib.sc_gilbert_baseline(
+            self.h, gap_tol, max_iters, ctypes.byref(v), ctypes.byref(g), ctypes.byref(it),
+            _ptr(mu), _ptr(gam)), "sc_gilbert_baseline")
+        return float(v.value), float(g.value), int(it.value), mu, gam
 
     def read_rows(self, first: int = 0, count: Optional[int] = None) -> np.ndarray:
         if count is None:

@@ -331,6 +331,13 @@ int sc_set_range(sc_handle* h, double D) {
     return SC_OK;
 }
 
+// the verification baselines are device-only; the emulator only exports the symbols
+int sc_meb_baseline(sc_handle*, int64_t, double*, double*) { return SC_EARG; }
+int sc_gilbert_baseline(sc_handle*, double, int64_t, double*, double*, int64_t*, double*,
+                        double*) {
+    return SC_EARG;
+}
+
 int sc_read_rows(sc_handle* h, int64_t first, int64_t count, double* out) {
     if (!h || !out || first < 0 || count < 0 || first + count > h->prob.n_local) return SC_EARG;
     const int d = h->prob.d;

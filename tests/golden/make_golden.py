@@ -7,6 +7,7 @@ it writes under tests/golden/ are committed and are what the tests read.
     python tests/golden/make_golden.py quick      # KATs, generators, traces, small solves
     python tests/golden/make_golden.py calls      # per-call solve_ftp/refine_run records
     python tests/golden/make_golden.py long       # C1 and n=2000 solves, threads 1/2/4/8
+    python tests/golden/make_golden.py baselines  # meb_baseline / gilbert_baseline records
 
 Instances are NOT stored: tests regenerate them from (n, d, seed, dist) with
 paper_2405_09157_b200.instances, whose bit-exactness against the reference
@@ -339,12 +340,50 @@ def gen_long(which=None):
             dump("long.json", out)
 
 
+# ---------------------------------------------------------------- verification baselines
+# (kind, instance args, radii seed or None, solver args); the radii, when present, are
+# drawn as rng(seed).uniform(0, 0.1, n)
+BASE_CASES = [
+    ("meb", (300, 4, 1, "gaussian"), None, {"eps_base": 0.05}),
+    ("meb", (200, 7, 2, "uniform-ball"), 11, {"eps_base": 0.1}),
+    ("meb", (64, 3, 0, "sphere-surface"), None, {"eps_base": 0.1}),
+    ("gilbert", (150, 120, 5, 3, 0.5), None, {"gap_tol": 1e-6, "max_iters": 100_000}),
+    ("gilbert", (80, 90, 3, 4, 0.1), None, {"gap_tol": 1e-8, "max_iters": 2000}),
+    ("gilbert", (40, 30, 12, 5, 2.0), None, {"gap_tol": 1e-10, "max_iters": 50_000}),
+]
+
+
+def gen_baselines():
+    from symcone import baselines
+    out = []
+    for kind, args, rseed, kw in BASE_CASES:
+        if kind == "meb":
+            inst = instances.gen_ses(*args)
+            rad = (np.random.default_rng(rseed).uniform(0.0, 0.1, args[0])
+                   if rseed is not None else None)
+            r = baselines.meb_baseline(inst.centers, rad, **kw)
+            out.append({"kind": kind, "inst": list(args), "radii_seed": rseed, "kw": kw,
+                        "value": _f(r.value), "center": _v(r.certificate),
+                        "iterations": int(r.iterations)})
+        else:
+            inst, _ = instances.gen_svm(*args)
+            r = baselines.gilbert_baseline(inst.P, inst.Q, **kw)
+            mu, gam = r.certificate
+            out.append({"kind": kind, "inst": list(args), "kw": kw, "value": _f(r.value),
+                        "gap": _f(r.gap), "iterations": int(r.iterations),
+                        "mu": _v(mu), "gam": _v(gam)})
+        print(kind, args, out[-1]["value"], out[-1]["iterations"], file=sys.stderr)
+    dump("baselines.json", out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "quick"
     if what == "quick":
         gen_generators()
         gen_kats()
         gen_traces()
+    elif what == "baselines":
+        gen_baselines()
     elif what == "calls":
         gen_calls()
     elif what == "long":
