@@ -11,6 +11,7 @@ impractical (80 GB at C5).
 from __future__ import annotations
 
 import io
+import os
 
 import numpy as np
 
@@ -131,7 +132,24 @@ def parse(text: str) -> SesInstance | SvmInstance:
     raise InstanceFormatError(f"unknown problem kind {head[0]!r}")
 
 
-def load(path: str) -> SesInstance | SvmInstance:
+def _is_npy_dir(path: str) -> bool:
+    return path.endswith(".npyd") or (os.path.isdir(path) and (
+        os.path.exists(os.path.join(path, "centers.npy")) or
+        os.path.exists(os.path.join(path, "P.npy"))))
+
+
+def load(path: str, mmap: bool = True) -> SesInstance | SvmInstance:
+    """Text (the reference's format, R/instances.py:1-9), ``.npz``, or a binary instance
+    directory (``*.npyd``: centers.npy + radii.npy, or P.npy + Q.npy).  Directories are
+    memory-mapped by default: an instance larger than host RAM streams from the page
+    cache through the engine's pinned staging buffers at upload."""
+    if _is_npy_dir(path):
+        mode = "r" if mmap else None
+        if os.path.exists(os.path.join(path, "centers.npy")):
+            return SesInstance(centers=np.load(os.path.join(path, "centers.npy"), mmap_mode=mode),
+                               radii=np.load(os.path.join(path, "radii.npy"), mmap_mode=mode))
+        return SvmInstance(P=np.load(os.path.join(path, "P.npy"), mmap_mode=mode),
+                           Q=np.load(os.path.join(path, "Q.npy"), mmap_mode=mode))
     if path.endswith(".npz"):
         z = np.load(path)
         if "centers" in z:
@@ -142,6 +160,15 @@ def load(path: str) -> SesInstance | SvmInstance:
 
 
 def save(path: str, inst_or_text) -> None:
+    if path.endswith(".npyd"):
+        os.makedirs(path, exist_ok=True)
+        if isinstance(inst_or_text, SesInstance):
+            np.save(os.path.join(path, "centers.npy"), inst_or_text.centers)
+            np.save(os.path.join(path, "radii.npy"), inst_or_text.radii)
+        else:
+            np.save(os.path.join(path, "P.npy"), inst_or_text.P)
+            np.save(os.path.join(path, "Q.npy"), inst_or_text.Q)
+        return
     if path.endswith(".npz"):
         if isinstance(inst_or_text, SesInstance):
             np.savez(path, centers=inst_or_text.centers, radii=inst_or_text.radii)

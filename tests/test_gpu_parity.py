@@ -238,3 +238,17 @@ def test_full_size_svm_properties(cuda_engine):
     assert P.close(r.best_progress, ro.best_progress, 1e-9)
     assert P.close(r.best_counter, ro.best_counter, 1e-9)
     dev.close()
+
+
+def test_memory_mapped_instance_solves_identically(cuda_engine, tmp_path):
+    """A binary instance directory, memory-mapped and uploaded through the pageable
+    staging path, gives the bit-identical solve of the in-memory instance."""
+    inst = instances.gen_ses(20_000, 20, 4, "uniform-ball")
+    path = str(tmp_path / "c.npyd")
+    instances.save(path, inst)
+    mapped = instances.load(path)
+    assert not mapped.centers.flags.owndata
+    r1, s1 = ses.solve_ses(inst, 1e-2, engine=cuda_engine)
+    r2, s2 = ses.solve_ses(mapped, 1e-2, engine=cuda_engine)
+    assert r1.total_iterations == r2.total_iterations
+    assert s1.radius == s2.radius and np.array_equal(s1.center, s2.center)

@@ -40,6 +40,22 @@ def test_instance_text_round_trip(tmp_path):
     assert np.array_equal(b2.P, s.P)
 
 
+def test_binary_instance_dir_round_trip(tmp_path):
+    """.npyd directories: exact round trip, memory-mapped on load."""
+    inst = instances.gen_ses(50, 4, 2, "gaussian")
+    inst = ses.SesInstance(centers=inst.centers, radii=np.linspace(0.0, 0.1, 50))
+    p = str(tmp_path / "a.npyd")
+    instances.save(p, inst)
+    back = instances.load(p)
+    assert not back.centers.flags.owndata     # a view of the file mapping, no copy
+    assert np.array_equal(back.centers, inst.centers) and np.array_equal(back.radii, inst.radii)
+    s, _ = instances.gen_svm(6, 9, 3, 1)
+    q = str(tmp_path / "b.npyd")
+    instances.save(q, s)
+    b2 = instances.load(q, mmap=False)
+    assert np.array_equal(b2.P, s.P) and np.array_equal(b2.Q, s.Q)
+
+
 @pytest.mark.parametrize("text", ["", "ses 2", "ses 2 1\n1 2\n", "foo 1 2\n", "svm 1 1 1\n1\n",
                                   "ses 2 1\n1 0\nnan 0\n"])
 def test_instance_parse_errors(text):
