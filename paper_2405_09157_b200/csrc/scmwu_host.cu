@@ -384,59 +384,6 @@ __global__ void __launch_bounds__(256) gilbert_kernel(const double* X, int ld, i
     }
 }
 
-// -------------------------------------------------------------------------------------
-// Per-SM streaming-rate calibration (one CTA per SM, all SMs streaming at once): every
-// CTA pulls its own `per` bytes through per-warp bulk-copy rings, the persistent kernel's
-// pattern, and records its cycles and SM id.  On B200 the rates differ by SM position
-// (measured: the first TPC of every 16-SM group ~25% faster than the rest, the others
-// within ~10% of each other; tools/die_probe.cu, profiles/r01_overhead.md).
-__global__ void __launch_bounds__(256, 1) calib_kernel(const char* X, size_t per, int tile,
-                                                       int S, long long* cyc, int* smid) {
-    extern __shared__ __align__(128) unsigned char csm[];
-    constexpr int W = 8;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(csm);
-    unsigned char* ring = csm + 1024;
-    const char* base = X + (size_t)blockIdx.x * per;
-    const int ntiles = (int)(per / tile);
-    if (lane == 0)
-        for (int s = 0; s < S; ++s) mbar_init(&bars[w * S + s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-    const long long t0 = clock64();
-    const int mine = (ntiles - w + W - 1) / W;
-    auto issue = [&](int q, int st) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_tx(&bars[w * S + st], (uint32_t)tile);
-        bulk_g2s(ring + (size_t)(w * S + st) * tile, base + (size_t)(w + q * W) * tile,
-                 (uint32_t)tile, &bars[w * S + st]);
-    };
-    if (lane == 0)
-        for (int q = 0; q < S && q < mine; ++q) issue(q, q);
-    int issued = min(S, mine), s_issue = issued % S, s = 0;
-    uint32_t phase = 0;
-    double acc = 0.0;
-    for (int q = 0; q < mine; ++q) {
-        mbar_wait(&bars[w * S + s], phase);
-        acc += reinterpret_cast<const double*>(ring + (size_t)(w * S + s) * tile)[lane];
-        __syncwarp();
-        if (issued < mine) {
-            if (lane == 0) issue(issued, s_issue);
-            ++issued;
-            s_issue = s_issue + 1 == S ? 0 : s_issue + 1;
-        }
-        if (++s == S) { s = 0; phase ^= 1u; }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        cyc[blockIdx.x] = clock64() - t0 + (acc == 1.2345 ? 1 : 0);
-        unsigned sm;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-        smid[blockIdx.x] = (int)sm;
-    }
-}
-
-
 }  // namespace scmwu
 
 // ======================================================================================
@@ -522,6 +469,10 @@ struct sc_handle {
     std::vector<double> red0_h;
     bool has_sep = false, has_callmin = false;
     bool by_smid = false;            // rows balanced per SM (configure)
+    bool balance_ok = false;         // eligible for the balanced partition (configure)
+    bool calib_tried = false;        // the calibration probe ran for this handle
+    int grid_req = 0;
+    std::vector<int64_t> cta_h;      // host copy of the partition {r0, r1, stride} per slot
     std::string err;
 };
 
@@ -535,65 +486,29 @@ static int cuda_fail(sc_handle* h, cudaError_t e, const char* what) {
         if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
     } while (0)
 
-// Per-device SM weights from calib_kernel, measured once per process and shared by every
-// handle on that device (so two handles of the same instance partition rows identically
-// and give bit-identical results).  Weights are the streaming rates quantised to 1/64 of
-// the fastest SM, which keeps the partition stable against timing noise.  Empty: no
-// balancing (SCMWU_BALANCE=0, SM ids not 0..#SMs-1, or the probe could not run).
+// Row partition balanced per SM (one CTA per SM).  B200 SMs do not stream at the same
+// rate: per-SM pass times of the persistent kernel spread by ~15 % and repeat run to run
+// to < 1 % (tools/die_probe.cu, profiles/r01_overhead.md), so with an equal partition the
+// first grid barrier absorbs the slowest SM's excess every pass.  The kernel itself is the
+// calibration: the first sc_ftp of a large single-GPU handle runs a short refine probe
+// with the equal cyclic partition, reads every SM's streaming cycles for its tiles and
+// derives per-SM throughput weights (quantised to 1/1024 of the fastest).  They are cached
+// per (device, kernel) for the process, so every later handle of that kernel partitions
+// identically (bitwise-reproducible results within a process).  SCMWU_BALANCE=0 disables.
+// (A pure streaming probe, tools/die_probe.cu, overshoots: it measures bandwidth shares, while
+// the SES pass is partly compute bound: SES C2 136 -> 149 us/pass.)
 static std::mutex g_calib_mu;
-static std::map<int, std::vector<double>> g_calib;
+static std::map<std::pair<int, const void*>, std::vector<double>> g_calib;
 
-static const std::vector<double>& sm_weights(sc_handle* h) {
-    std::lock_guard<std::mutex> lock(g_calib_mu);
-    const int dev = h->prob.device;
-    auto it = g_calib.find(dev);
-    if (it != g_calib.end()) return it->second;
-    std::vector<double>& w = g_calib[dev];
-    // opt-in (SCMWU_BALANCE=1): the probe's pure-streaming rates overshoot for the compute
-    // loaded passes (SES C2 136 -> 149 us/pass, SVM C3 137 -> 135.5, same box), so the
-    // default keeps the equal cyclic partition
+static bool balance_enabled() {
     const char* e = getenv("SCMWU_BALANCE");
-    if (e == nullptr || atoi(e) == 0) return w;
-    const int G = h->sms, S = 2, tile = 13312;
-    const size_t per = (size_t)tile * 8 * 48;          // 48 tiles per warp (~5 MB per SM)
-    char* buf = nullptr;
-    long long* cyc = nullptr;
-    int* sid = nullptr;
-    if (cudaMalloc(&buf, per * G) != cudaSuccess) { cudaGetLastError(); return w; }
-    bool ok = cudaMalloc(&cyc, G * sizeof(long long)) == cudaSuccess &&
-              cudaMalloc(&sid, G * sizeof(int)) == cudaSuccess &&
-              cudaMemsetAsync(buf, 0, per * G, h->stream) == cudaSuccess;
-    const int smem = 1024 + 8 * S * tile;
-    ok = ok && cudaFuncSetAttribute(calib_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem) == cudaSuccess;
-    std::vector<long long> best(G, 0);
-    std::vector<long long> hc(G);
-    std::vector<int> hs(G);
-    for (int rep = 0; ok && rep < 4; ++rep) {
-        calib_kernel<<<G, 256, smem, h->stream>>>(buf, per, tile, S, cyc, sid);
-        ok = cudaStreamSynchronize(h->stream) == cudaSuccess &&
-             cudaMemcpy(hc.data(), cyc, G * sizeof(long long), cudaMemcpyDeviceToHost) ==
-                 cudaSuccess &&
-             cudaMemcpy(hs.data(), sid, G * sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess;
-        if (!ok || rep == 0) continue;                   // rep 0 warms up
-        for (int b = 0; b < G; ++b) {
-            if (hs[b] < 0 || hs[b] >= G) { ok = false; break; }
-            long long& m = best[hs[b]];
-            m = m == 0 ? hc[b] : std::min(m, hc[b]);
-        }
-    }
-    h->launches += 4;
-    if (buf) cudaFree(buf);
-    if (cyc) cudaFree(cyc);
-    if (sid) cudaFree(sid);
-    cudaGetLastError();
-    for (int s = 0; ok && s < G; ++s) ok = best[s] > 0;   // every SM id seen
-    if (!ok) return w;
-    const long long fastest = *std::min_element(best.begin(), best.end());
-    w.resize(G);
-    for (int s = 0; s < G; ++s)
-        w[s] = std::max(1.0, std::round(64.0 * (double)fastest / (double)best[s])) / 64.0;
-    return w;
+    return e == nullptr || atoi(e) != 0;
+}
+
+static const std::vector<double>* sm_weights(sc_handle* h) {
+    std::lock_guard<std::mutex> lock(g_calib_mu);
+    auto it = g_calib.find({h->prob.device, (const void*)h->fn});
+    return it == g_calib.end() ? nullptr : &it->second;
 }
 
 // tiles [0, T) of one side split over `slots` contiguous blocks in proportion to the
@@ -661,9 +576,13 @@ static int configure(sc_handle* h, int grid_req) {
     std::vector<int64_t> cta(3 * (size_t)G);
     // one CTA per SM: contiguous tile blocks per SM id sized by the SM's measured rate
     h->by_smid = false;
-    if (G == h->sms) {
-        const std::vector<double>& w = sm_weights(h);
-        if ((int)w.size() == G) {
+    h->grid_req = grid_req;
+    const bool big = n / tr >= (int64_t)64 * G;   // >= 64 tiles per SM: worth balancing
+    h->balance_ok = G == h->sms && big && h->prob.world <= 1 && balance_enabled();
+    if (h->balance_ok) {
+        const std::vector<double>* wp = sm_weights(h);
+        if (wp != nullptr && (int)wp->size() == G) {
+            const std::vector<double>& w = *wp;
             h->by_smid = true;
             auto fill = [&](int s0, int s1, int64_t rs, int64_t re) {
                 const int64_t T = (re - rs + tr - 1) / tr;
@@ -721,6 +640,7 @@ static int configure(sc_handle* h, int grid_req) {
     h->smem = need(S);
     if (h->smem > (size_t)kMaxSmem) { h->err = "shared memory budget exceeded"; return SC_EARG; }
     h->grid = G;
+    h->cta_h = cta;
     if (h->row_begin) cudaFree(h->row_begin);
     if (h->partials) cudaFree(h->partials);
     CK(cudaMalloc(&h->row_begin, cta.size() * sizeof(int64_t)), "alloc rows");
@@ -1002,8 +922,8 @@ int sc_set_grid(sc_handle* h, int32_t grid) {
     return configure(h, grid);
 }
 
-int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_tilde,
-           double* best_y) {
+static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
+                    double* y_tilde, double* best_y, long long* slot_cycles) {
     if (!h || !args || !res || !y_tilde || !best_y) return SC_EARG;
     memset(res, 0, sizeof(*res));
     if (args->mode != SC_MODE_FTP && args->mode != SC_MODE_REFINE) return SC_EARG;
@@ -1042,6 +962,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     p.wrap_prefetch = getenv("SCMWU_DEFER_PREFETCH") ? 0 : 1;
     p.flush_after_tail = getenv("SCMWU_FLUSH_AFTER_TAIL") ? 1 : 0;
     p.by_smid = h->by_smid ? 1 : 0;
+    p.slot_cycles = slot_cycles;
     p.X = h->X; p.radii = h->radii; p.row_begin = h->row_begin;
     p.rho = h->prob.rho; p.inv_rho = 1.0 / h->prob.rho; p.R = h->prob.R; p.ln_r = h->prob.ln_r;
     p.D = h->prob.D; p.g1 = h->g1;
@@ -1092,6 +1013,78 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     if (status == SC_EWIDTH) { h->err = "width violation"; return SC_EWIDTH; }
     if (status != SC_OK) { h->err = "kernel did not complete"; return SC_ECUDA; }
     return SC_OK;
+}
+
+// Balanced-partition calibration (see sm_weights): a refine run at the feasible end of
+// the range (never separates) with the equal partition, per-SM cycles per tile -> weights.
+// The handle's call state is restored afterwards (slots, pass counter, pd flags).
+static void calibrate_partition(sc_handle* h) {
+    h->calib_tried = true;
+    const int G = h->grid;
+    sc_ftp_args a;
+    memset(&a, 0, sizeof(a));
+    a.mode = SC_MODE_REFINE;
+    a.has_progress = 1;
+    a.alpha = h->prob.kind == SC_SES ? h->prob.D : 1e-3 * h->prob.D;
+    a.ceil_ln_r = (int64_t)ceil(h->prob.ln_r);
+    a.horizon = std::max<int64_t>(24, a.ceil_ln_r);
+    a.delta = 1e-4;
+    a.patience = 10;
+    a.enabled = 0;
+    a.gain_rel = 1e-4;
+    a.lo = -INFINITY;
+    a.hi = INFINITY;
+    a.target = NAN;
+    long long* dc = nullptr;
+    if (!(a.alpha > 0.0) || cudaMalloc(&dc, 2 * (size_t)G * sizeof(long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    sc_ftp_result r;
+    std::vector<double> yt(h->dd), by(h->dd);
+    const int st = ftp_impl(h, &a, &r, yt.data(), by.data(), dc);
+    std::vector<long long> hc(2 * (size_t)G);
+    const bool ok = st == SC_OK && r.passes >= 16 &&
+                    cudaMemcpy(hc.data(), dc, hc.size() * 8, cudaMemcpyDeviceToHost) ==
+                        cudaSuccess;
+    cudaFree(dc);
+    // restore the call state the probe touched
+    cudaMemset(h->slots, 0, (size_t)kNumSlots * h->slot_len * 8);
+    h->has_sep = h->has_callmin = false;
+    h->pass_total = 0;
+    h->err.clear();
+    if (!ok) { cudaGetLastError(); return; }
+    std::vector<double> thr(G, 0.0);
+    for (int b = 0; b < G; ++b) {
+        const int64_t c0 = h->cta_h[3 * b], c1 = h->cta_h[3 * b + 1], sd = h->cta_h[3 * b + 2];
+        const int64_t tiles = c1 > c0 ? (c1 - c0 + sd - 1) / sd : 0;
+        const long long cyc = hc[2 * b], sm = hc[2 * b + 1];
+        if (sm < 0 || sm >= G || cyc <= 0 || tiles <= 0 || thr[sm] != 0.0) return;   // no map
+        thr[sm] = (double)tiles / (double)cyc;
+    }
+    const double mx = *std::max_element(thr.begin(), thr.end());
+    std::vector<double> w(G);
+    for (int s = 0; s < G; ++s) w[s] = std::max(1.0, std::round(1024.0 * thr[s] / mx)) / 1024.0;
+    {
+        std::lock_guard<std::mutex> lock(g_calib_mu);
+        g_calib.emplace(std::make_pair(h->prob.device, (const void*)h->fn), w);
+    }
+    configure(h, h->grid_req);
+}
+
+int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_tilde,
+           double* best_y) {
+    if (!h || !args || !res || !y_tilde || !best_y) return SC_EARG;
+    if (h->balance_ok && !h->by_smid && !h->calib_tried) {
+        CK(cudaSetDevice(h->prob.device), "set device");
+        if (sm_weights(h) != nullptr) {   // another handle of this kernel calibrated
+            h->calib_tried = true;
+            configure(h, h->grid_req);
+        } else {
+            calibrate_partition(h);
+        }
+    }
+    return ftp_impl(h, args, res, y_tilde, best_y, nullptr);
 }
 
 int sc_progress_parts(sc_handle* h, const double* y, double* out) {

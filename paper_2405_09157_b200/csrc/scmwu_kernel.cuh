@@ -135,6 +135,7 @@ struct KParams {
     int wrap_prefetch;                 // 1: prefetch the next pass during the reduction
     int flush_after_tail;              // 1: issue the next pass's copies after the tail
     int by_smid;                       // 1: work slot = SM id (G == #SMs, balanced rows)
+    long long* slot_cycles;            // optional: per slot {streaming cycles, SM id}
     int64_t n, n1;
     const double* X;           // n x ld (ld even, padded with zeros)
     const double* radii;       // SES: n rounded up to even (zero padded)
@@ -962,8 +963,12 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     unsigned long long g_start = 0, g_end = 0, g_arr = 0, g_rel = 0;
 #endif
     int64_t width_passes = 0;
+    // partition calibration (p.slot_cycles set): this slot's streaming cycles over all
+    // passes (thread 0; pass start to the CTA join)
+    long long scyc = 0, scyc0 = 0;
     while (pp->action == kPass) {
         const PassParams ps = *pp;
+        if (p.slot_cycles != nullptr && tid == 0) scyc0 = clock64();
 #ifdef SCMWU_PHASE_TIMING
         if (tid == 0) {
             tcta0 = clock64();
@@ -981,6 +986,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         }
         SCMWU_TMARK(0)
         consumer_sync();
+        if (p.slot_cycles != nullptr && tid == 0) scyc += clock64() - scyc0;
 #ifdef SCMWU_PHASE_TIMING
         // per-CTA streaming time (all CTAs): the skew the first grid barrier absorbs
         if (tid == 0 && p.timing != nullptr) {
@@ -1147,6 +1153,12 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     if (p.timing != nullptr && b == 0 && tid == 0)
         for (int i = 0; i < 8; ++i) p.timing[16 + 960 + i] = tt_sh[i];
 #endif
+    if (p.slot_cycles != nullptr && tid == 0) {
+        unsigned s;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s));
+        p.slot_cycles[2 * slot] = scyc;
+        p.slot_cycles[2 * slot + 1] = (long long)s;
+    }
     // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
     stream_drain(p, m, warp, ws);
     if (b == 0 && warp == 0) {

@@ -1,3 +1,4 @@
+# same-box A/B of the calibrated per-SM partition (SCMWU_BALANCE=0 vs default)
 for rep in 1 2; do
  for mode in 0 1; do
   export SCMWU_BALANCE=$mode

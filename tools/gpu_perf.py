@@ -61,6 +61,9 @@ def main():
             G = dev.handle.info()["grid"]
             per = full[9:9 + G] / max(r.passes, 1)
             sm = full[169:169 + G]
+            if os.environ.get("SCMWU_DUMP"):
+                with open(os.environ["SCMWU_DUMP"], "w") as fh:
+                    json.dump({"cycles_per_pass": per.tolist(), "smid": sm.tolist()}, fh)
             if per.max() > 0:
                 order = np.argsort(per)
                 print(f"  per-CTA streaming cycles/pass: min {per.min():.0f} median "
