@@ -586,8 +586,13 @@ static int configure(sc_handle* h, int grid_req) {
             h->by_smid = true;
             auto fill = [&](int s0, int s1, int64_t rs, int64_t re) {
                 const int64_t T = (re - rs + tr - 1) / tr;
-                const std::vector<int64_t> cnt =
-                    weighted_split(T, std::vector<double>(w.begin() + s0, w.begin() + s1));
+                // whole groups of kNW tiles per SM, so its 8 warps get equal tile counts
+                // (the CTA join waited up to one tile time); the < kNW leftover tiles go
+                // to the slots one each, from the first
+                std::vector<int64_t> cnt = weighted_split(
+                    T / kNW, std::vector<double>(w.begin() + s0, w.begin() + s1));
+                for (auto& c : cnt) c *= kNW;
+                for (int64_t r = 0; r < T % kNW; ++r) ++cnt[(size_t)(r % cnt.size())];
                 int64_t t0 = 0;
                 for (int i = 0; i < s1 - s0; ++i) {
                     const int s = s0 + i;
@@ -646,7 +651,7 @@ static int configure(sc_handle* h, int grid_req) {
     CK(cudaMalloc(&h->row_begin, cta.size() * sizeof(int64_t)), "alloc rows");
     CK(cudaMemcpy(h->row_begin, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
        "copy rows");
-    CK(cudaMalloc(&h->partials, (size_t)G * h->rw * sizeof(double)), "alloc partials");
+    CK(cudaMalloc(&h->partials, 2 * (size_t)G * h->rw * sizeof(double)), "alloc partials");
     CK(cudaFuncSetAttribute(h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem),
        "smem attribute");
     int per_sm = 0;

@@ -142,7 +142,7 @@ struct KParams {
     const int64_t* row_begin;  // per CTA {first row, end row, row stride of its warp tiles}
     double rho, inv_rho, R, ln_r, D, g1;
     const double* red0;        // reduced vector of iterate 1 (all logits 0)
-    double* partials;          // G x rw
+    double* partials;          // 2 (pass parity) x G x rw
     double* redg;              // rw
     unsigned long long* bar;   // grid barrier counter (zeroed per launch)
     double* ring;
@@ -825,8 +825,40 @@ static __device__ __noinline__ void rank_exchange(const KParams& p, double* red,
     }
 }
 
+// Every CTA folds all G partials itself (one grid barrier per pass instead of two): warp w
+// sums the contiguous partial range [w*G/8, (w+1)*G/8) lane-per-column (its loads issue
+// ahead of the adds), then the 8 range sums are combined in warp order.  Columns go in
+// chunks of the warp-partial scratch (pws doubles per warp).  The order is fixed and the
+// same in every CTA, so all CTAs hold identical reduced vectors.
 template <int KIND>
-static __device__ __noinline__ void fold_all(const KParams& p, double* red, bool publish) {
+static __device__ __noinline__ void fold_redundant(const KParams& p, const SmemMap& m,
+                                                   const double* part, int pws) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q0 = warp * p.G / kNW, q1 = (warp + 1) * p.G / kNW;
+    for (int c0 = 0; c0 < p.rw; c0 += pws) {
+        const int c1 = min(p.rw, c0 + pws);
+        for (int j = c0 + lane; j < c1; j += 32) {
+            const int op = red_op(KIND, j);
+            double acc = op_identity(op);
+#pragma unroll 8
+            for (int q = q0; q < q1; ++q)
+                acc = op_apply(op, acc, __ldcg(part + (size_t)q * p.rw + j));
+            m.wpart[warp * pws + (j - c0)] = acc;
+        }
+        consumer_sync();
+        for (int j = c0 + (int)threadIdx.x; j < c1; j += kNW * 32) {
+            const int op = red_op(KIND, j);
+            double acc = op_identity(op);
+            for (int w = 0; w < kNW; ++w) acc = op_apply(op, acc, m.wpart[w * pws + (j - c0)]);
+            m.red[j] = acc;
+        }
+        consumer_sync();
+    }
+}
+
+template <int KIND>
+static __device__ __noinline__ void fold_all(const KParams& p, const double* part, double* red,
+                                            bool publish) {
     constexpr int FC = 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j0 = warp * FC; j0 < p.rw; j0 += kNW * FC) {
@@ -838,7 +870,7 @@ static __device__ __noinline__ void fold_all(const KParams& p, double* red, bool
             acc[k] = op_identity(op[k]);
         }
         for (int q = lane; q < p.G; q += 32) {
-            const double* row = p.partials + (size_t)q * p.rw;
+            const double* row = part + (size_t)q * p.rw;
 #pragma unroll
             for (int k = 0; k < FC; ++k)
                 if (j0 + k < p.rw) acc[k] = op_apply(op[k], acc[k], __ldcg(row + j0 + k));
@@ -996,7 +1028,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         }
 #endif
         SCMWU_TMARK(1)
-        // CTA partial, fixed warp order, written in the reduced layout
+        // CTA partial, fixed warp order, written in the reduced layout (partials are
+        // double-buffered by pass parity for the single-barrier redundant fold)
+        double* const part = p.partials + (size_t)(pass_idx & 1) * p.G * p.rw;
         const int nw_act = nwt < kNW ? nwt : kNW;   // warps that own at least one tile
         for (int j = tid; j < p.rw; j += kNW * 32) {
             double v;
@@ -1018,7 +1052,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
                     v = acc;
                 }
             }
-            p.partials[(size_t)slot * p.rw + j] = v;
+            part[(size_t)slot * p.rw + j] = v;
         }
         SCMWU_TMARK(2)
         if (kFoldVariants && p.fold_mode == kFoldLast) {
@@ -1034,7 +1068,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             consumer_sync();
             SCMWU_TMARK(3)
             if (m.flags[0]) {
-                fold_all<KIND>(p, m.red, true);
+                fold_all<KIND>(p, part, m.red, true);
                 SCMWU_TMARK(4)
                 consumer_sync();
                 if (tid == 0)
@@ -1053,13 +1087,14 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             }
             consumer_sync();
             SCMWU_TMARK(6)
-        } else if (kFoldVariants && p.fold_mode == kFoldRedundant) {
+        } else if (p.fold_mode == kFoldRedundant && !(kMultiGpu && p.world > 1)) {
             // every CTA folds all G partials itself with the same fixed tree
+            // one barrier: the partials are double-buffered by pass parity, and a CTA can
+            // run at most one pass ahead of the slowest reader
             grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
             SCMWU_TMARK(3)
-            fold_all<KIND>(p, m.red, false);
+            fold_redundant<KIND>(p, m, part, pws);
             SCMWU_TMARK(4)
-            consumer_sync();
             SCMWU_TMARK(6)
         } else {
 #ifdef SCMWU_PHASE_TIMING
@@ -1080,7 +1115,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
 #pragma unroll
                 for (int i = 0; i < 5; ++i) {
                     const int q = lane + 32 * i;
-                    ld[i] = q < p.G ? __ldcg(p.partials + (size_t)q * p.rw + j) : 0.0;
+                    ld[i] = q < p.G ? __ldcg(part + (size_t)q * p.rw + j) : 0.0;
                 }
 #pragma unroll
                 for (int i = 0; i < 5; ++i)
