@@ -206,7 +206,7 @@ def reference_arm(args, w, rank):
     for _ in range(args.warmup):
         cpu_sample(w, inst, max_seconds=3.0, max_iters=1)
     for _ in range(args.steps):
-        samples.append(cpu_sample(w, inst, max_seconds=20.0))
+        samples.append(cpu_sample(w, inst, max_seconds=args.cpu_seconds))
     spi = statistics.median(s["s_per_iter"] for s in samples)
     iters = ITERS_EST[args.workload]
     value = spi * iters
@@ -238,7 +238,7 @@ def reference_arm_scaled(args, w):
         cpu_sample(ws, warm, max_seconds=1.0, max_iters=1)
     spis = []
     for _ in range(args.steps):
-        spi, desc = cpu_scaled(w, 20.0)
+        spi, desc = cpu_scaled(w, args.cpu_seconds)
         spis.append(spi)
     spi = statistics.median(spis)
     bpp = alg_bytes_per_pass(w)
