@@ -1020,11 +1020,12 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     return SC_OK;
 }
 
-// Balanced-partition calibration (see sm_weights): a refine run at the feasible end of
-// the range (never separates) with the equal partition, per-SM cycles per tile -> weights.
-// The handle's call state is restored afterwards (slots, pass counter, pd flags).
-static void calibrate_partition(sc_handle* h) {
-    h->calib_tried = true;
+// Balanced-partition calibration (see sm_weights): refine runs at the feasible end of the
+// range (they never separate) report every SM's streaming cycles for its tiles.  Round 1
+// runs with the equal cyclic partition; round 2 re-measures under the weighted partition
+// (loading an SM's GPC changes its rate) and replaces the weights.  The handle's call
+// state is restored afterwards (slots, pass counter, pd flags).
+static bool probe_throughput(sc_handle* h, std::vector<double>& thr) {
     const int G = h->grid;
     sc_ftp_args a;
     memset(&a, 0, sizeof(a));
@@ -1043,7 +1044,7 @@ static void calibrate_partition(sc_handle* h) {
     long long* dc = nullptr;
     if (!(a.alpha > 0.0) || cudaMalloc(&dc, 2 * (size_t)G * sizeof(long long)) != cudaSuccess) {
         cudaGetLastError();
-        return;
+        return false;
     }
     sc_ftp_result r;
     std::vector<double> yt(h->dd), by(h->dd);
@@ -1058,23 +1059,36 @@ static void calibrate_partition(sc_handle* h) {
     h->has_sep = h->has_callmin = false;
     h->pass_total = 0;
     h->err.clear();
-    if (!ok) { cudaGetLastError(); return; }
-    std::vector<double> thr(G, 0.0);
+    if (!ok) { cudaGetLastError(); return false; }
+    thr.assign(G, 0.0);
     for (int b = 0; b < G; ++b) {
         const int64_t c0 = h->cta_h[3 * b], c1 = h->cta_h[3 * b + 1], sd = h->cta_h[3 * b + 2];
         const int64_t tiles = c1 > c0 ? (c1 - c0 + sd - 1) / sd : 0;
         const long long cyc = hc[2 * b], sm = hc[2 * b + 1];
-        if (sm < 0 || sm >= G || cyc <= 0 || tiles <= 0 || thr[sm] != 0.0) return;   // no map
+        if (sm < 0 || sm >= G || cyc <= 0 || tiles <= 0 || thr[sm] != 0.0) return false;
         thr[sm] = (double)tiles / (double)cyc;
     }
-    const double mx = *std::max_element(thr.begin(), thr.end());
-    std::vector<double> w(G);
-    for (int s = 0; s < G; ++s) w[s] = std::max(1.0, std::round(1024.0 * thr[s] / mx)) / 1024.0;
-    {
-        std::lock_guard<std::mutex> lock(g_calib_mu);
-        g_calib.emplace(std::make_pair(h->prob.device, (const void*)h->fn), w);
+    return true;
+}
+
+static void calibrate_partition(sc_handle* h) {
+    h->calib_tried = true;
+    const int G = h->grid;
+    const auto key = std::make_pair(h->prob.device, (const void*)h->fn);
+    std::vector<double> thr;
+    for (int round = 0; round < 2; ++round) {
+        if (!probe_throughput(h, thr)) break;
+        const double mx = *std::max_element(thr.begin(), thr.end());
+        std::vector<double> w(G);
+        for (int s = 0; s < G; ++s)
+            w[s] = std::max(1.0, std::round(1024.0 * thr[s] / mx)) / 1024.0;
+        {
+            std::lock_guard<std::mutex> lock(g_calib_mu);
+            g_calib[key] = w;
+        }
+        configure(h, h->grid_req);
+        if (!h->by_smid) break;
     }
-    configure(h, h->grid_req);
 }
 
 int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_tilde,
