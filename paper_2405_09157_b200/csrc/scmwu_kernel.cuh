@@ -224,6 +224,9 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
         while (ld_acquire(bar) < target) {
+#if defined(SCMWU_POLL_NS) && SCMWU_POLL_NS > 0
+            __nanosleep(SCMWU_POLL_NS);   // A/B: back off instead of hammering the L2 line
+#endif
         }
     }
     consumer_sync();
