@@ -18,7 +18,7 @@ if python bench.py --workload "$wl" --steps 1 --warmup 1 --no-cpu-baseline > /de
     python bench.py --workload "$wl" --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
   # one full capture of a persistent-kernel launch (a mid-solve sc_ftp call)
   timeout 1500 ncu --set full --import-source on --clock-control none -k regex:scmwu_kernel \
-    -s 4 -c 1 -o $out/full_${tag}_${wl} \
+    -s 20 -c 1 -o $out/full_${tag}_${wl} \
     python bench.py --workload "$wl" --steps 1 --warmup 1 --no-cpu-baseline > $out/ncu_${tag}_${wl}.log 2>&1
 fi
 ls -la $out | grep "$tag"
