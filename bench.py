@@ -58,6 +58,10 @@ WORKLOADS = {
                             "on the device; per-iteration HBM GB/s over a 64-iteration "
                             "refine run"),
 }
+# Read-only streaming ceiling of the kernel's own access pattern on B200 (per-warp bulk-copy
+# rings, no math; tools/stream_bench.cu, profiles/r01_overhead.md).  MEASURED_PEAKS.json's
+# hbm_gbs is a copy (read + write) figure; a read-only kernel can exceed it.
+READ_CEILING_GBS = 7400.0
 # GPU iteration counts of full solves measured by this bench (profiles/); used only by the
 # reference arm to extrapolate the CPU port's s/iter to a time-to-eps.
 ITERS_EST = {"ses_c2": 15_515, "svm_c3": 320_146, "ses_c1": 103_672, "ses_c4": 360_000}
@@ -390,6 +394,8 @@ def our_arm(args, w, rank, world):
                     "enclosure_slack": sol0.enclosure_slack} if w["kind"] == "ses" else
                    {"margin": sol0.margin, "pd_distance": sol0.pd_distance}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "read_ceiling": READ_CEILING_GBS,
+                     "frac_of_read_ceiling": achieved / READ_CEILING_GBS,
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_pass": alg_bytes_per_pass(w),
                      "us_per_pass": kernel_s / passes * 1e6 if passes else None,
@@ -539,6 +545,8 @@ def gen_arm(args, w, rank, world):
                    "iterations": iters, "generate_s": gen_s,
                    "l2": "inputs larger than L2 (X = %.0f MB)" % (bpp / 1e6), "kernel": info},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "read_ceiling": READ_CEILING_GBS,
+                     "frac_of_read_ceiling": achieved / READ_CEILING_GBS,
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_pass": bpp,
                      "us_per_pass": kernel_s / passes * 1e6 if passes else None,
