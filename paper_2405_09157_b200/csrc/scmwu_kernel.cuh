@@ -508,19 +508,21 @@ __device__ __forceinline__ void stream_drain(const KParams& p, const SmemMap& m,
 // after which lane (grp, l) holds the complete sums of row (l / DUP) * RPW + grp
 // (DUP = LPR / NB identical copies), so the per-row scalar math (sqrt, exp, div) runs
 // once per lane for NB * RPW rows instead of once per lane group.
+// Select-free: the caller stores row-group k ^ (l / DUP) in slot k (an XOR permutation
+// per lane), so at every level ALL lanes keep slot i and send slot i + half — the
+// partner's slot i + half then holds the same row-group as my slot i — and slot 0 ends
+// with row-group l / DUP.  Same pairs, same operand order as the select form: the sums
+// are bit-identical, without 2 selects per value per level.
 template <int LPR, int NB, int V>
 __device__ __forceinline__ void reduce_scatter(double (&v)[V][NB], int l) {
+    (void)l;
 #pragma unroll
     for (int lev = 0, o = LPR / 2, half = NB / 2; half >= 1; ++lev, o >>= 1, half >>= 1) {
-        const bool up = (l & o) != 0;
 #pragma unroll
         for (int s = 0; s < V; ++s) {
 #pragma unroll
-            for (int i = 0; i < half; ++i) {
-                const double send = up ? v[s][i] : v[s][i + half];
-                const double keep = up ? v[s][i + half] : v[s][i];
-                v[s][i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
+            for (int i = 0; i < half; ++i)
+                v[s][i] = v[s][i] + __shfl_xor_sync(0xffffffffu, v[s][i + half], o);
         }
     }
 #pragma unroll
@@ -579,7 +581,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         double dfk[NB][CPL];
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            const int r = k * RPW + grp;
+            const int r = (k ^ myk) * RPW + grp;   // slot k: row-group k ^ myk
             const double* xr = xs + (size_t)(r < nr ? r : 0) * ld + l;
             double sa = 0, sl = 0, sw = 0, sf = 0;
 #pragma unroll
@@ -635,7 +637,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         // (zero in the unused column slots)
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            const double ck = __shfl_sync(0xffffffffu, cc, grp * LPR + k * DUP);
+            const double ck = __shfl_sync(0xffffffffu, cc, grp * LPR + (k ^ myk) * DUP);
 #pragma unroll
             for (int c = 0; c < CPL; ++c) Sd[c] = fma(ck, dfk[k][c], Sd[c]);
         }
@@ -707,7 +709,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
         double xk[NB][CPL];   // the staged rows, kept in registers for the G update
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            const int r = k * RPW + grp;
+            const int r = (k ^ myk) * RPW + grp;   // slot k: row-group k ^ myk
             const double* xr = xs + (size_t)(r < nr ? r : 0) * ld + l;
             double dW = 0, dw = 0, dy = 0, dz = 0;
 #pragma unroll
@@ -752,7 +754,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
         }
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            const double ek = __shfl_sync(0xffffffffu, e, grp * LPR + k * DUP);
+            const double ek = __shfl_sync(0xffffffffu, e, grp * LPR + (k ^ myk) * DUP);
 #pragma unroll
             for (int c = 0; c < CPL; ++c) G[c] = fma(ek, xk[k][c], G[c]);
         }
