@@ -136,6 +136,7 @@ struct KParams {
     int flush_after_tail;              // 1: issue the next pass's copies after the tail
     int by_smid;                       // 1: work slot = SM id (G == #SMs, balanced rows)
     long long* slot_cycles;            // optional: per slot {streaming cycles, SM id}
+    double l2_frac;                    // fraction of every CTA's tiles kept in L2 (0: off)
     int64_t n, n1;
     const double* X;           // n x ld (ld even, padded with zeros)
     const double* radii;       // SES: n rounded up to even (zero padded)
@@ -203,6 +204,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
         "[%3];" ::"r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+// the same copy with an L2 eviction-priority hint (createpolicy): rows kept in L2 across
+// passes use evict_last, the streamed remainder evict_first
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* b, bool keep) {
+    uint64_t pol;
+    if (keep)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
         : "memory");
 }
 __device__ __forceinline__ void consumer_sync() {
@@ -397,13 +413,15 @@ struct WarpStream {
     int s_issue;      // stage the next copy goes to (tiles fill stages cyclically)
     int inflight;     // issued and not yet consumed
     int64_t tstride;  // rows between this CTA's consecutive warp tiles
+    int keep;         // tiles [0, keep) of this CTA are loaded with an L2 evict_last hint
 };
 
 __device__ __forceinline__ void issue_tile(const KParams& p, const SmemMap& m, int64_t r0,
-                                           int64_t r1, int64_t tstride, int w, int q,
+                                           int64_t r1, const WarpStream& ws, int w, int q,
                                            int stage) {
     const int slot = w * p.stages + stage;
-    const int64_t a = r0 + (int64_t)(w + q * kNW) * tstride;
+    const int j = w + q * kNW;                    // this CTA's tile index
+    const int64_t a = r0 + (int64_t)j * ws.tstride;
     const int64_t b = min(r1, a + (int64_t)p.tile_rows);
     unsigned char* dst = m.ring + (size_t)slot * p.stage_stride;
     const uint32_t xb = (uint32_t)((b - a) * p.ld * 8);
@@ -416,6 +434,14 @@ __device__ __forceinline__ void issue_tile(const KParams& p, const SmemMap& m, i
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_tx(&m.full[slot], bytes);
+    if (ws.keep > 0) {   // the CTA's first `keep` tiles stay in L2 across passes
+        const bool keep = j < ws.keep;
+        bulk_g2s_hint(dst, p.X + a * p.ld, xb, &m.full[slot], keep);
+        if (p.kind == SC_SES)
+            bulk_g2s_hint(dst + p.rad_off, p.radii + ra, (uint32_t)((rb - ra) * 8),
+                          &m.full[slot], keep);
+        return;
+    }
     bulk_g2s(dst, p.X + a * p.ld, xb, &m.full[slot]);
     if (p.kind == SC_SES)
         bulk_g2s(dst + p.rad_off, p.radii + ra, (uint32_t)((rb - ra) * 8), &m.full[slot]);
@@ -428,7 +454,7 @@ __device__ __forceinline__ void stream_start(const KParams& p, const SmemMap& m,
     ws.phase = 0;
     const int first = ws.cnt < p.stages ? ws.cnt : p.stages;
     if ((threadIdx.x & 31) == 0)
-        for (int q = 0; q < first; ++q) issue_tile(p, m, r0, r1, ws.tstride, w,q, q);
+        for (int q = 0; q < first; ++q) issue_tile(p, m, r0, r1, ws, w,q, q);
     ws.issued = first;
     ws.deferred = 0;
     ws.inflight = first;
@@ -449,7 +475,7 @@ __device__ __forceinline__ void stream_flush(const KParams& p, const SmemMap& m,
     }
     if ((threadIdx.x & 31) == 0)
         for (int q = 0; q < ws.deferred; ++q) {
-            issue_tile(p, m, r0, r1, ws.tstride, w,q, ws.s_issue);
+            issue_tile(p, m, r0, r1, ws, w,q, ws.s_issue);
             ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
         }
     else
@@ -478,12 +504,12 @@ __device__ __forceinline__ void release_stage(const KParams& p, const SmemMap& m
     __syncwarp();
     --ws.inflight;
     if (ws.issued < ws.cnt) {            // the next tile of this pass
-        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, ws.tstride, w,ws.issued, ws.s_issue);
+        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, ws, w,ws.issued, ws.s_issue);
         ++ws.issued;
         ++ws.inflight;
         ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
     } else if (p.wrap_prefetch) {        // (A/B) prefetch the next pass right away
-        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, ws.tstride, w,ws.deferred, ws.s_issue);
+        if ((threadIdx.x & 31) == 0) issue_tile(p, m, r0, r1, ws, w,ws.deferred, ws.s_issue);
         ++ws.deferred;
         ++ws.inflight;
         ws.s_issue = ws.s_issue + 1 == p.stages ? 0 : ws.s_issue + 1;
@@ -927,6 +953,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     __syncthreads();
     WarpStream ws;
     ws.tstride = tstride;
+    ws.keep = (int)((double)nwt * p.l2_frac);
     stream_start(p, m, r0, r1, warp, ws, nwt);
 
     // ------------------------------------------------------------ consumers
