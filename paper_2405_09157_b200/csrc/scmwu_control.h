@@ -214,7 +214,7 @@ struct Control {
 #if defined(__CUDA_ARCH__) && defined(SCMWU_PHASE_TIMING)
         if (tt != nullptr && L::lane() == 0) {
             const long long now = clock64();
-            if (i > 0) tt[i] += now - tt_prev;
+            if (i > 0 && tt_prev != 0) tt[i] += now - tt_prev;
             tt_prev = now;
         }
 #else
