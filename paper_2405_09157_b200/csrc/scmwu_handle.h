@@ -1,0 +1,63 @@
+// scmwu_handle.h — the engine handle shared by the host translation units
+// (scmwu_host.cu: lifecycle, partition, feasibility tests; scmwu_baselines.cu: the
+// verification baselines).  Private: not part of the C ABI.
+#pragma once
+
+#include "scmwu_kernel.cuh"
+
+using namespace scmwu;
+
+struct LaunchCfg {
+    int lpr, cpl, nb;
+};
+
+struct sc_handle {
+    sc_problem prob;
+    int dd, ld, rw, pw, slot_len;
+    LaunchCfg cfg;
+    int sms = 0, grid = 0, gP = 0, tile_rows = 0, stages = 0, resident = 0;
+    uint32_t stage_stride = 0, rad_off = 0;
+    size_t smem = 0;
+    KernelFn fn = nullptr;
+    double g1 = 0.0;
+    double last_alpha = 0.0;
+    // device buffers
+    double *X = nullptr, *radii = nullptr, *red0 = nullptr, *partials = nullptr, *redg = nullptr;
+    int64_t* row_begin = nullptr;
+    unsigned long long* bar = nullptr;
+    double* ring = nullptr;
+    int64_t ring_cap = 0;
+    double* slots = nullptr;
+    sc_ftp_result* res = nullptr;
+    double *y_tilde = nullptr, *best_y = nullptr, *scratch = nullptr, *yvec = nullptr;
+    int* status = nullptr;
+    long long* timing = nullptr;     // SCMWU_TIMING=1: per-phase cycle sums of the last call
+    double* v1 = nullptr;            // SES anchor row
+    // sharding: this rank's mailbox (flags + 2 x world x rw doubles) and the peers'
+    void* mbox_base = nullptr;
+    void* peer_base[kMaxWorld] = {};
+    bool connected = false;
+    int64_t pass_total = 0;          // passes of all previous calls (identical on all ranks)
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, mk0 = nullptr, mk1 = nullptr;
+    int64_t launches = 0;
+    // host state
+    std::vector<double> red0_h;
+    bool has_sep = false, has_callmin = false;
+    bool by_smid = false;            // rows balanced per SM (configure)
+    bool balance_ok = false;         // eligible for the balanced partition (configure)
+    bool calib_tried = false;        // the calibration probe ran for this handle
+    int grid_req = 0;
+    std::vector<int64_t> cta_h;      // host copy of the partition {r0, r1, stride} per slot
+    std::string err;
+};
+
+inline int cuda_fail(sc_handle* h, cudaError_t e, const char* what) {
+    if (h) h->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? SC_EOOM : SC_ECUDA;
+}
+#define CK(call, what)                                   \
+    do {                                                 \
+        cudaError_t _e = (call);                         \
+        if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
+    } while (0)
