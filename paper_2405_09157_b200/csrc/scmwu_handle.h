@@ -45,6 +45,7 @@ struct sc_handle {
     std::vector<double> red0_h;
     bool has_sep = false, has_callmin = false;
     bool by_smid = false;            // rows balanced per SM (configure)
+    int vworld = 0;                  // tests: emulated ranks on this GPU (SCMWU_VWORLD)
     bool balance_ok = false;         // eligible for the balanced partition (configure)
     bool calib_tried = false;        // the calibration probe ran for this handle
     int grid_req = 0;

@@ -299,25 +299,16 @@ static int configure(sc_handle* h, int grid_req) {
     const int64_t step = (int64_t)kNW * RPW;
     if (grid_req <= 0) G = (int)std::min<int64_t>(G, std::max<int64_t>(1, (n + step - 1) / step));
     const int64_t n1 = h->prob.kind == SC_SVM ? h->prob.n1_local : 0, n2 = n - n1;
+    (void)d;
     const bool two_sided = h->prob.kind == SC_SVM && n1 > 0 && n2 > 0;
+    // emulated ranks (tests, SCMWU_VWORLD): W groups of G / W CTAs, one per rank
+    const int W = h->vworld > 1 ? h->vworld : 1;
     if (two_sided) G = std::max(G, 2);
     G = std::min(G, h->sms);
     G = std::min(G, 160);   // the column fold loads at most 5 partials per lane
+    if (W > 1) G = std::max(2 * W, G / W * W);
     if (G < 1) G = 1;
     if (two_sided && G < 2) { h->err = "SVM needs >= 2 SMs"; return SC_EARG; }
-    // rows -> CTAs (SVM: P-CTAs then Q-CTAs, each CTA single-sided)
-    std::vector<int64_t> rb(G + 1);
-    if (h->prob.kind == SC_SES || !two_sided) {
-        for (int b = 0; b <= G; ++b) rb[b] = (int64_t)((__int128)n * b / G) & ~(int64_t)1;
-        rb[G] = n;
-        h->gP = h->prob.kind == SC_SVM && n1 > 0 ? G : 0;   // one-sided SVM shard
-    } else {
-        int gP = (int)llround((double)G * (double)n1 / (double)n);
-        gP = std::max(1, std::min(G - 1, gP));
-        for (int b = 0; b <= gP; ++b) rb[b] = (int64_t)((__int128)n1 * b / gP);
-        for (int b = gP; b <= G; ++b) rb[b] = n1 + (int64_t)((__int128)n2 * (b - gP) / (G - gP));
-        h->gP = gP;
-    }
     // warp tiles: NB row-groups of RPW rows; one SW-stage ring per consumer warp
     const int64_t rowb = (int64_t)h->ld * 8;
     const int tr = h->cfg.nb * RPW;
@@ -326,68 +317,72 @@ static int configure(sc_handle* h, int grid_req) {
     h->rad_off = (xb + 15) & ~15u;
     const uint32_t radb = h->prob.kind == SC_SES ? (uint32_t)((tr + 2) * 8) : 0u;
     h->stage_stride = (h->rad_off + radb + 127) & ~127u;
-    // per-CTA tile sequence {first row, end row, row stride between its warp tiles}.
-    // Cyclic (default): CTA c of a side with g CTAs takes that side's tiles c, c+g, ...,
-    // so every CTA streams from the whole address range (per-CTA pass times were 13-18%
-    // apart with contiguous blocks on some boxes, growing with the block's address,
-    // profiles/r01_overhead.md).  SCMWU_CONTIG=1: contiguous blocks.
-    const bool cyclic = getenv("SCMWU_CONTIG") == nullptr;
-    std::vector<int64_t> cta(3 * (size_t)G);
-    // one CTA per SM: contiguous tile blocks per SM id sized by the SM's measured rate
+    // Partition: per slot {first row, end row, row stride between its warp tiles, SVM P}.
+    // Within a side (SVM: P rows then Q rows, every CTA single-sided) the tiles are dealt
+    // cyclically: slot c of a side with g slots takes tiles c, c+g, ... (every CTA streams
+    // from the whole address range).  Large single-GPU handles switch to contiguous blocks
+    // per SM id sized by the calibrated per-SM rates (see sm_weights).
+    std::vector<int64_t> cta(4 * (size_t)G, 0);
     h->by_smid = false;
     h->grid_req = grid_req;
     const bool big = n / tr >= (int64_t)64 * G;   // >= 64 tiles per SM: worth balancing
-    h->balance_ok = G == h->sms && big && h->prob.world <= 1 && balance_enabled();
-    if (h->balance_ok) {
-        const std::vector<double>* wp = sm_weights(h);
-        if (wp != nullptr && (int)wp->size() == G) {
-            const std::vector<double>& w = *wp;
-            h->by_smid = true;
-            auto fill = [&](int s0, int s1, int64_t rs, int64_t re) {
-                const int64_t T = (re - rs + tr - 1) / tr;
-                // whole groups of kNW tiles per SM, so its 8 warps get equal tile counts
-                // (the CTA join waited up to one tile time); the < kNW leftover tiles go
-                // to the slots one each, from the first
-                std::vector<int64_t> cnt = weighted_split(
-                    T / kNW, std::vector<double>(w.begin() + s0, w.begin() + s1));
-                for (auto& c : cnt) c *= kNW;
-                for (int64_t r = 0; r < T % kNW; ++r) ++cnt[(size_t)(r % cnt.size())];
-                int64_t t0 = 0;
-                for (int i = 0; i < s1 - s0; ++i) {
-                    const int s = s0 + i;
-                    cta[3 * s] = rs + t0 * tr;
-                    cta[3 * s + 1] = std::min(re, rs + (t0 + cnt[i]) * tr);
-                    cta[3 * s + 2] = tr;
-                    t0 += cnt[i];
-                }
-            };
-            if (two_sided) {
-                fill(0, h->gP, 0, n1);
-                fill(h->gP, G, n1, n);
-            } else {
-                fill(0, G, 0, n);
+    h->balance_ok = G == h->sms && big && h->prob.world <= 1 && W == 1 && balance_enabled();
+    const std::vector<double>* wp = h->balance_ok ? sm_weights(h) : nullptr;
+    if (wp != nullptr && (int)wp->size() == G) h->by_smid = true;
+    auto deal = [&](int s0, int s1, int64_t rs, int64_t re, bool P) {
+        if (s1 <= s0) return;
+        if (h->by_smid) {
+            const int64_t T = (re - rs + tr - 1) / tr;
+            // whole groups of kNW tiles per SM, so its 8 warps get equal tile counts; the
+            // < kNW leftover tiles go to the slots one each, from the first
+            std::vector<int64_t> cnt = weighted_split(
+                T / kNW, std::vector<double>(wp->begin() + s0, wp->begin() + s1));
+            for (auto& c : cnt) c *= kNW;
+            for (int64_t r = 0; r < T % kNW; ++r) ++cnt[(size_t)(r % cnt.size())];
+            int64_t t0 = 0;
+            for (int i = 0; i < s1 - s0; ++i) {
+                const int sl = s0 + i;
+                cta[4 * sl] = rs + t0 * tr;
+                cta[4 * sl + 1] = std::min(re, rs + (t0 + cnt[i]) * tr);
+                cta[4 * sl + 2] = tr;
+                cta[4 * sl + 3] = P ? 1 : 0;
+                t0 += cnt[i];
             }
+            return;
+        }
+        const int g = s1 - s0;
+        for (int i = 0; i < g; ++i) {
+            const int sl = s0 + i;
+            cta[4 * sl] = rs + (int64_t)i * tr;
+            cta[4 * sl + 1] = re;
+            cta[4 * sl + 2] = (int64_t)g * tr;
+            cta[4 * sl + 3] = P ? 1 : 0;
+        }
+    };
+    const int Gv = G / W;
+    h->gP = 0;
+    for (int r = 0; r < W; ++r) {
+        // rank r's rows: the np.array_split rule of the real sharding (shard.row_ranges)
+        const int64_t q = n / W, m = n % W;
+        const int64_t R0 = r * q + std::min<int64_t>(r, m), R1 = R0 + q + (r < m ? 1 : 0);
+        const int s0 = r * Gv, s1 = s0 + Gv;
+        if (h->prob.kind == SC_SES) { deal(s0, s1, R0, R1, false); continue; }
+        const int64_t p0 = R0, p1 = std::min(R1, std::max(R0, n1));   // P rows of the rank
+        if (p1 > p0 && R1 > p1) {
+            int gp = (int)llround((double)Gv * (double)(p1 - p0) / (double)(R1 - R0));
+            gp = std::max(1, std::min(Gv - 1, gp));
+            deal(s0, s0 + gp, p0, p1, true);
+            deal(s0 + gp, s1, p1, R1, false);
+            if (r == 0) h->gP = gp;
+        } else {
+            deal(s0, s1, R0, R1, p1 > p0);
+            if (r == 0 && p1 > p0) h->gP = Gv;
         }
     }
     int nwt = 0;
-    for (int b = 0; b < G; ++b) {
-        int64_t c0, c1, st;
-        if (h->by_smid) {
-            c0 = cta[3 * b]; c1 = cta[3 * b + 1]; st = cta[3 * b + 2];
-        } else if (!cyclic) {
-            c0 = rb[b]; c1 = rb[b + 1]; st = tr;
-        } else {
-            int64_t s0 = 0, s1 = n;
-            int gc = G, ci = b;
-            if (two_sided) {
-                const bool P = b < h->gP;
-                s0 = P ? 0 : n1; s1 = P ? n1 : n;
-                gc = P ? h->gP : G - h->gP; ci = P ? b : b - h->gP;
-            }
-            c0 = s0 + (int64_t)ci * tr; c1 = s1; st = (int64_t)gc * tr;
-        }
-        cta[3 * b] = c0; cta[3 * b + 1] = c1; cta[3 * b + 2] = st;
-        const int t = c1 > c0 ? (int)((c1 - c0 + st - 1) / st) : 0;
+    for (int sl = 0; sl < G; ++sl) {
+        const int64_t c0 = cta[4 * sl], c1 = cta[4 * sl + 1], st = cta[4 * sl + 2];
+        const int t = c1 > c0 && st > 0 ? (int)((c1 - c0 + st - 1) / st) : 0;
         nwt = std::max(nwt, t);
     }
     const int per_warp = (nwt + kNW - 1) / kNW;
@@ -600,10 +595,58 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
            "copy colsum");
         cudaFree(cs);
     }
+    // Emulated ranks on one GPU (tests only, SCMWU_VWORLD = 2..8 with world <= 1): the
+    // iterate-1 vector is the rank-ordered fold of the ranks' local vectors, exactly as a
+    // sharded solve builds it (shard.fold_ranks), and every rank gets a mailbox in this
+    // GPU's memory; the kernel then runs the real exchange code between CTA groups.
+    if (const char* e = getenv("SCMWU_VWORLD")) {
+        const int W = atoi(e);
+        if (W > 1 && W <= kMaxWorld && P.world <= 1 && n >= 2 * W) {
+            h->vworld = W;
+            std::vector<double> acc(h->rw);
+            for (int j = 0; j < h->rw; ++j) {
+                const int op = red_op(prob->kind, j);
+                acc[j] = op_identity(op);
+            }
+            double* cs = nullptr;
+            CK(cudaMalloc(&cs, 2 * (size_t)d * 8), "alloc colsum");
+            for (int r = 0; r < W; ++r) {
+                const int64_t q = n / W, m = n % W;
+                const int64_t R0 = r * q + std::min<int64_t>(r, m), R1 = R0 + q + (r < m ? 1 : 0);
+                std::vector<double> loc(h->rw, 0.0);
+                if (prob->kind == SC_SES) {
+                    double rad = 0.0;
+                    const int64_t first = R0 == 0 ? 1 : 0;
+                    if (radii)
+                        for (int64_t i = R0 + first; i < R1; ++i) rad += 2.0 * radii[i];
+                    loc[kS_T] = 2.0 * (double)(R1 - R0 - first);
+                    loc[kS_Rad] = rad;
+                } else {
+                    const int64_t p1 = std::min(R1, std::max(R0, P.n1_local));
+                    loc[kV_TP] = (double)(p1 - R0);
+                    loc[kV_TQ] = (double)(R1 - p1);
+                    colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, R0, p1, d, h->ld, cs);
+                    colsum_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(h->X, p1, R1, d, h->ld,
+                                                                           cs + d);
+                    CK(cudaStreamSynchronize(h->stream), "colsum");
+                    CK(cudaMemcpy(loc.data() + kV_Vec, cs, 2 * (size_t)d * 8,
+                                  cudaMemcpyDeviceToHost), "copy colsum");
+                }
+                for (int j = 0; j < h->rw; ++j) acc[j] = op_apply(red_op(prob->kind, j), acc[j], loc[j]);
+            }
+            cudaFree(cs);
+            h->red0_h = acc;
+            // mailboxes of all emulated ranks: [flags 64 | data 2 x W x rw] each
+            const size_t mb = 64 * 8 + 2 * (size_t)W * h->rw * 8;
+            CK(cudaMalloc(&h->mbox_base, mb * W), "alloc mailboxes");
+            CK(cudaMemset(h->mbox_base, 0, mb * W), "zero mailboxes");
+            for (int r = 0; r < W; ++r) h->peer_base[r] = static_cast<char*>(h->mbox_base) + mb * r;
+        }
+    }
     CK(cudaMalloc(&h->red0, h->rw * 8), "alloc red0");
     CK(cudaMemcpy(h->red0, h->red0_h.data(), h->rw * 8, cudaMemcpyHostToDevice), "copy red0");
     CK(cudaMalloc(&h->redg, h->rw * 8), "alloc redg");
-    CK(cudaMalloc(&h->bar, 64), "alloc barrier");
+    CK(cudaMalloc(&h->bar, 1024), "alloc barrier");   // + one counter per emulated rank
     CK(cudaMalloc(&h->slots, (size_t)kNumSlots * h->slot_len * 8), "alloc slots");
     CK(cudaMemset(h->slots, 0, (size_t)kNumSlots * h->slot_len * 8), "zero slots");
     CK(cudaMalloc(&h->res, sizeof(sc_ftp_result)), "alloc result");
@@ -753,6 +796,13 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     p.shard = h->prob.shard;
     p.row0 = h->prob.row0;
     p.pass_base = h->pass_total;
+    p.vworld = h->vworld;
+    if (h->vworld > 1) {
+        for (int r = 0; r < h->vworld; ++r) {
+            p.mflag[r] = reinterpret_cast<unsigned long long*>(h->peer_base[r]);
+            p.mbox[r] = reinterpret_cast<double*>(static_cast<char*>(h->peer_base[r]) + 64 * 8);
+        }
+    }
     if (p.world > 1) {
         if (!h->connected) { h->err = "sharded handle is not connected (sc_connect)"; return SC_EARG; }
         for (int r = 0; r < p.world; ++r) {
@@ -760,7 +810,7 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
             p.mbox[r] = reinterpret_cast<double*>(static_cast<char*>(h->peer_base[r]) + 64 * 8);
         }
     }
-    CK(cudaMemsetAsync(h->bar, 0, 64, h->stream), "reset barrier");
+    CK(cudaMemsetAsync(h->bar, 0, 1024, h->stream), "reset barrier");
     CK(cudaMemsetAsync(h->res, 0, sizeof(sc_ftp_result), h->stream), "reset result");
     CK(cudaMemsetAsync(h->status, 0xff, sizeof(int), h->stream), "reset status");
     void* kargs[] = {&p};
@@ -830,7 +880,7 @@ static bool probe_throughput(sc_handle* h, std::vector<double>& thr) {
     if (!ok) { cudaGetLastError(); return false; }
     thr.assign(G, 0.0);
     for (int b = 0; b < G; ++b) {
-        const int64_t c0 = h->cta_h[3 * b], c1 = h->cta_h[3 * b + 1], sd = h->cta_h[3 * b + 2];
+        const int64_t c0 = h->cta_h[4 * b], c1 = h->cta_h[4 * b + 1], sd = h->cta_h[4 * b + 2];
         const int64_t tiles = c1 > c0 ? (c1 - c0 + sd - 1) / sd : 0;
         const long long cyc = hc[2 * b], sm = hc[2 * b + 1];
         if (sm < 0 || sm >= G || cyc <= 0 || tiles <= 0 || thr[sm] != 0.0) return false;
@@ -1095,7 +1145,7 @@ void sc_destroy(sc_handle* h) {
     void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar, h->timing,
                     h->ring, h->slots, h->res, h->y_tilde, h->best_y, h->scratch, h->yvec,
                     h->status, h->v1, h->mbox_base};
-    for (int r = 0; r < kMaxWorld; ++r)
+    for (int r = 0; r < kMaxWorld && h->vworld <= 1; ++r)   // emulated ranks: own memory
         if (h->peer_base[r] && h->peer_base[r] != h->mbox_base) cudaIpcCloseMemHandle(h->peer_base[r]);
     for (void* b : bufs)
         if (b) cudaFree(b);

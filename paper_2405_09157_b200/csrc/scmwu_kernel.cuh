@@ -137,10 +137,11 @@ struct KParams {
     int by_smid;                       // 1: work slot = SM id (G == #SMs, balanced rows)
     long long* slot_cycles;            // optional: per slot {streaming cycles, SM id}
     double l2_frac;                    // fraction of every CTA's tiles kept in L2 (0: off)
+    int vworld;                        // > 1: emulate that many ranks on this GPU (tests)
     int64_t n, n1;
     const double* X;           // n x ld (ld even, padded with zeros)
     const double* radii;       // SES: n rounded up to even (zero padded)
-    const int64_t* row_begin;  // per CTA {first row, end row, row stride of its warp tiles}
+    const int64_t* row_begin;  // per slot {first row, end row, tile stride, SVM P side}
     double rho, inv_rho, R, ln_r, D, g1;
     const double* red0;        // reduced vector of iterate 1 (all logits 0)
     double* partials;          // 2 (pass parity) x G x rw
@@ -266,7 +267,7 @@ __host__ __device__ __forceinline__ int red_op(int kind, int j) {
 __host__ __device__ __forceinline__ double op_identity(int op) {
     return op == kSum ? 0.0 : (op == kMax ? -INFINITY : INFINITY);
 }
-__device__ __forceinline__ double op_apply(int op, double a, double b) {
+__host__ __device__ __forceinline__ double op_apply(int op, double a, double b) {
     return op == kSum ? a + b : (op == kMax ? fmax(a, b) : fmin(a, b));
 }
 // SVM: the partial column (one side) feeding reduced column j, and which side owns it
@@ -825,33 +826,64 @@ enum FoldMode { kFoldTwoBarriers = 0, kFoldRedundant = 1, kFoldLast = 2 };
 // the rank vectors in rank order into `red`.  Flags are monotone pass counters across
 // calls (no reset race); a 2^37-cycle timeout reports a missing peer via flags[1].
 // Out of line: it must not cost the streaming loop registers.
+// The rank a CTA belongs to.  Real multi-GPU (world > 1): every CTA of this GPU is rank
+// `shard`.  Emulated ranks on one GPU (vworld > 1, tests): the grid is split into vworld
+// groups of G / vworld CTAs, each group a rank with its own rows, barrier counter and
+// mailbox, all running the same exchange code as real ranks do.
+struct RankGroup {
+    int W;                       // ranks (1: single GPU)
+    int rank;
+    int G;                       // CTAs of this rank
+    int first;                   // its first CTA index
+    unsigned long long* bar;     // its grid-barrier counter
+};
+
+__device__ __forceinline__ RankGroup rank_group(const KParams& p, int b) {
+    RankGroup g;
+    if (p.vworld > 1) {
+        g.W = p.vworld;
+        g.G = p.G / p.vworld;
+        g.rank = b / g.G;
+        g.first = g.rank * g.G;
+        g.bar = p.bar + 8 * (g.rank + 1);
+    } else {
+        g.W = p.world > 1 ? p.world : 1;
+        g.rank = p.world > 1 ? p.shard : 0;
+        g.G = p.G;
+        g.first = 0;
+        g.bar = p.bar;
+    }
+    return g;
+}
+
 template <int KIND>
-static __device__ __noinline__ void rank_exchange(const KParams& p, double* red,
-                                                  volatile int* flags, int pass_idx) {
+static __device__ __noinline__ void rank_exchange(const KParams& p, const RankGroup g,
+                                                  double* red, volatile int* flags,
+                                                  int pass_idx) {
     const int tid = threadIdx.x;
     const unsigned long long want = (unsigned long long)(p.pass_base + pass_idx + 1);
-    if (tid == 0 && blockIdx.x == 0)
-        for (int r = 0; r < p.world; ++r)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[r] + p.shard),
+    if (tid == 0 && (int)blockIdx.x == g.first)
+        for (int r = 0; r < g.W; ++r)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[r] + g.rank),
                          "l"(want)
                          : "memory");
     if (tid == 0) {
         const long long t0 = clock64();
-        for (int r = 0; r < p.world; ++r) {
+        for (int r = 0; r < g.W; ++r) {
             unsigned long long v;
             do {
                 asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
-                             : "=l"(v) : "l"(p.mflag[p.shard] + r) : "memory");
+                             : "=l"(v) : "l"(p.mflag[g.rank] + r) : "memory");
                 if (clock64() - t0 > (1ll << 37)) { flags[1] = 1; break; }
             } while (v < want);
         }
     }
     consumer_sync();
-    const double* mb = p.mbox[p.shard] + (size_t)((p.pass_base + pass_idx) & 1) * p.world * p.rw;
+    const double* mb = p.mbox[g.rank] + (size_t)((p.pass_base + pass_idx) & 1) * g.W * p.rw;
     for (int j = tid; j < p.rw; j += kNW * 32) {
         const int op = red_op(KIND, j);
         double acc = op_identity(op);
-        for (int r = 0; r < p.world; ++r) acc = op_apply(op, acc, __ldcg(mb + (size_t)r * p.rw + j));
+        for (int r = 0; r < g.W; ++r) acc = op_apply(op, acc, __ldcg(mb + (size_t)r * p.rw + j));
         red[j] = acc;
     }
 }
@@ -940,10 +972,10 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         slot = (int)s;
     }
     // this slot's warp tiles: tile j covers rows [r0 + j * tstride, + tile_rows) below r1
-    const int64_t r0 = p.row_begin[3 * slot], r1 = p.row_begin[3 * slot + 1];
-    const int64_t tstride = p.row_begin[3 * slot + 2];
+    const int64_t r0 = p.row_begin[4 * slot], r1 = p.row_begin[4 * slot + 1];
+    const int64_t tstride = p.row_begin[4 * slot + 2];
     const int nwt = r1 > r0 ? (int)((r1 - r0 + tstride - 1) / tstride) : 0;
-    const bool isP = KIND == SC_SVM && slot < p.gP;
+    const bool isP = KIND == SC_SVM && p.row_begin[4 * slot + 3] != 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNW * p.stages; ++s) mbar_init(&m.full[s], 1);
         m.flags[0] = 0;
@@ -1005,7 +1037,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     int pass_idx = 0;
     unsigned long long nbar = 0;
     // columns of the reduced vector folded by this CTA
-    const int c0 = (int)((int64_t)b * p.rw / p.G), c1 = (int)((int64_t)(b + 1) * p.rw / p.G);
+    const RankGroup grp = rank_group(p, b);
+    const int lb = b - grp.first;                 // index of this CTA within its rank
+    const int c0 = (int)((int64_t)lb * p.rw / grp.G), c1 = (int)((int64_t)(lb + 1) * p.rw / grp.G);
     const int pws = (p.pw + 1) & ~1;
     // per-phase timing only in -DSCMWU_PHASE_TIMING builds: the nine live counters
     // would otherwise cost registers in the streaming loop of every build
@@ -1087,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             part[(size_t)slot * p.rw + j] = v;
         }
         SCMWU_TMARK(2)
-        if (kFoldVariants && p.fold_mode == kFoldLast) {
+        if (kFoldVariants && p.fold_mode == kFoldLast && grp.W <= 1) {
             // one global synchronisation: the CTA whose arrival completes the pass
             // folds all partials (fixed tree) and publishes them with a release epoch
             consumer_sync();
@@ -1119,11 +1153,11 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             }
             consumer_sync();
             SCMWU_TMARK(6)
-        } else if (p.fold_mode == kFoldRedundant && !(kMultiGpu && p.world > 1)) {
+        } else if (p.fold_mode == kFoldRedundant && grp.W <= 1) {
             // every CTA folds all G partials itself with the same fixed tree
             // one barrier: the partials are double-buffered by pass parity, and a CTA can
             // run at most one pass ahead of the slowest reader
-            grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
+            grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G);
             SCMWU_TMARK(3)
             fold_redundant<KIND>(p, m, part, pws);
             SCMWU_TMARK(4)
@@ -1133,12 +1167,14 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             consumer_sync();
             if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_arr));
 #endif
-            grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
+            grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G);
 #ifdef SCMWU_PHASE_TIMING
             if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_rel));
 #endif
             SCMWU_TMARK(3)
-            // column-distributed fold over the G partials: warp per column, fixed tree
+            // column-distributed fold over this rank's G partials: warp per column, fixed
+            // tree
+            const double* gpart = part + (size_t)grp.first * p.rw;
             for (int j = c0 + warp; j < c1; j += kNW) {
                 const int op = red_op(KIND, j);
                 double acc = op_identity(op);
@@ -1147,21 +1183,21 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
 #pragma unroll
                 for (int i = 0; i < 5; ++i) {
                     const int q = lane + 32 * i;
-                    ld[i] = q < p.G ? __ldcg(part + (size_t)q * p.rw + j) : 0.0;
+                    ld[i] = q < grp.G ? __ldcg(gpart + (size_t)q * p.rw + j) : 0.0;
                 }
 #pragma unroll
                 for (int i = 0; i < 5; ++i)
-                    if (lane + 32 * i < p.G) acc = op_apply(op, acc, ld[i]);
+                    if (lane + 32 * i < grp.G) acc = op_apply(op, acc, ld[i]);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1)
                     acc = op_apply(op, acc, __shfl_xor_sync(0xffffffffu, acc, o));
                 if (lane == 0) {
-                    if (kMultiGpu && p.world > 1) {
-                        // this rank's folded column -> slot [parity][shard] of EVERY
-                        // rank's mailbox (NVLink stores to the peers' HBM)
+                    if (kMultiGpu && grp.W > 1) {
+                        // this rank's folded column -> slot [parity][rank] of EVERY rank's
+                        // mailbox (NVLink stores to the peers' HBM)
                         const size_t off =
-                            ((size_t)((p.pass_base + pass_idx) & 1) * p.world + p.shard) * p.rw + j;
-                        for (int r = 0; r < p.world; ++r) p.mbox[r][off] = acc;
+                            ((size_t)((p.pass_base + pass_idx) & 1) * grp.W + grp.rank) * p.rw + j;
+                        for (int r = 0; r < grp.W; ++r) p.mbox[r][off] = acc;
                         __threadfence_system();
                     } else {
                         p.redg[j] = acc;
@@ -1169,10 +1205,10 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
                 }
             }
             SCMWU_TMARK(4)
-            grid_barrier(p.bar, (++nbar) * (unsigned long long)p.G);
+            grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G);
             SCMWU_TMARK(5)
-            if (kMultiGpu && p.world > 1) {
-                rank_exchange<KIND>(p, m.red, m.flags, pass_idx);
+            if (kMultiGpu && grp.W > 1) {
+                rank_exchange<KIND>(p, grp, m.red, m.flags, pass_idx);
             } else {
                 for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
             }
