@@ -862,21 +862,23 @@ static __device__ __noinline__ void rank_exchange(const KParams& p, const RankGr
                                                   int pass_idx) {
     const int tid = threadIdx.x;
     const unsigned long long want = (unsigned long long)(p.pass_base + pass_idx + 1);
-    if (tid == 0 && (int)blockIdx.x == g.first)
-        for (int r = 0; r < g.W; ++r)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[r] + g.rank),
-                         "l"(want)
-                         : "memory");
-    if (tid == 0) {
+    // thread r raises this rank's flag in rank r's mailbox and then waits for rank r's
+    // flag in ours, so the W release stores and the W acquire polls run in parallel
+    // (one thread doing them in sequence cost one system-scope round trip per rank).
+    // Ordering: the mailbox stores of every folding warp precede the grid barrier this
+    // CTA passed (thread 0's acquire + bar.sync), so thread r's release covers them.
+    if (tid < g.W && (int)blockIdx.x == g.first)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[tid] + g.rank),
+                     "l"(want)
+                     : "memory");
+    if (tid < g.W) {
         const long long t0 = clock64();
-        for (int r = 0; r < g.W; ++r) {
-            unsigned long long v;
-            do {
-                asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
-                             : "=l"(v) : "l"(p.mflag[g.rank] + r) : "memory");
-                if (clock64() - t0 > (1ll << 37)) { flags[1] = 1; break; }
-            } while (v < want);
-        }
+        unsigned long long v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+                         : "=l"(v) : "l"(p.mflag[g.rank] + tid) : "memory");
+            if (clock64() - t0 > (1ll << 37)) { flags[1] = 1; break; }
+        } while (v < want);
     }
     consumer_sync();
     const double* mb = p.mbox[g.rank] + (size_t)((p.pass_base + pass_idx) & 1) * g.W * p.rw;
