@@ -472,6 +472,11 @@ SC_UNROLL4
             save_state(s.pd_pending, v.ysum, cur);
             if (pend_buf != nullptr) keep_state(pend_buf, v.ysum, cur);
         }
+        if (win_len + 2 > s.ring_cap) {   // the window would overwrite live ring entries
+            finish_common();
+            status = SC_EOOM;
+            return kDone;
+        }
         double* slot = s.ring + pos_count * s.ring_stride;
         // SES width bound: with u_k = U_k / k the running average,
         //   |alpha - g_i| + |y_k - v_i| <= |alpha| + F(u_k) + |y_k - u_k|,

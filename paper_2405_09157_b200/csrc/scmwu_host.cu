@@ -744,7 +744,11 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     // window history: max(64, T/2) + 2 entries (the largest rung is <= T)
     int64_t need = std::max<int64_t>(kLadderBase, T / 2) + 2;
     const int dd8 = (h->dd + 1) & ~1;                             // 16-byte ring entries
-    const int64_t cap_lim = ((int64_t)1 << 30) / (dd8 * 8);       // 1 GiB
+    // capped at SCMWU_RING_GB (default 2 GiB: 2.6M entries at d = 100, 0.5M at d = 512); a run
+    // whose window outgrows the ring stops with SC_EOOM instead of overwriting live entries
+    double ring_gb = 2.0;
+    if (const char* e = getenv("SCMWU_RING_GB")) ring_gb = std::max(1e-6, atof(e));
+    const int64_t cap_lim = std::max<int64_t>(kLadderBase + 2, (int64_t)(ring_gb * 1073741824.0) / (dd8 * 8));
     if (need > cap_lim) need = cap_lim;
     if (need > h->ring_cap) {
         if (h->ring) cudaFree(h->ring);
@@ -833,6 +837,10 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     h->has_callmin = res->has_counter_min != 0;
     h->has_sep = res->kind == SC_PRIMAL;
     if (status == SC_EWIDTH) { h->err = "width violation"; return SC_EWIDTH; }
+    if (status == SC_EOOM) {
+        h->err = "the suffix window outgrew the window ring (raise SCMWU_RING_GB)";
+        return SC_EOOM;
+    }
     if (status != SC_OK) { h->err = "kernel did not complete"; return SC_ECUDA; }
     return SC_OK;
 }

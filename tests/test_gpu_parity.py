@@ -252,3 +252,21 @@ def test_memory_mapped_instance_solves_identically(cuda_engine, tmp_path):
     r2, s2 = ses.solve_ses(mapped, 1e-2, engine=cuda_engine)
     assert r1.total_iterations == r2.total_iterations
     assert s1.radius == s2.radius and np.array_equal(s1.center, s2.center)
+
+
+def test_window_ring_overflow_fails_loudly(cuda_engine, monkeypatch):
+    """A suffix window longer than the window ring must stop the call with SC_EOOM, not
+    overwrite live entries (SCMWU_RING_GB caps the ring)."""
+    from paper_2405_09157_b200 import _native as nat
+    inst = instances.gen_ses(3000, 10, 1, "gaussian")
+    D, _, _ = ses.ses_range(inst)
+    dev = ses.ses_device(inst, D, engine=cuda_engine)
+    spec = meta.OracleSpec(dev.cone, 3 * D / math.sqrt(2), inst.d + 1, dev, math.sqrt(2),
+                           meta.Orientation.MAX)
+    monkeypatch.setenv("SCMWU_RING_GB", "0.0001")      # ~1000 entries at d = 10
+    with pytest.raises(nat.NativeError, match="window ring"):
+        meta.refine_run(spec, D, 4000, meta.EarlyStopConfig(enabled=False), dev.progress)
+    monkeypatch.delenv("SCMWU_RING_GB")
+    r = meta.refine_run(spec, D, 4000, meta.EarlyStopConfig(enabled=False), dev.progress)
+    assert r.iterations == 4000
+    dev.close()
