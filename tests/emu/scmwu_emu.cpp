@@ -234,7 +234,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     h->last_alpha = args->alpha;
     // the ring holds at most max(64, T_rung/2)+1 live entries; the largest rung is <= T
     int64_t cap = (T / 2 > kLadderBase ? T / 2 : kLadderBase) + 2;
-    if (args->mode == SC_MODE_FTP && cap > (1 << 24)) cap = (1 << 24);
+    if (cap > (1 << 21)) cap = (1 << 21);   // longer windows stop with SC_EOOM (control)
     h->ring.assign((size_t)cap * dd, 0.0);
 
     std::vector<double> ysum(dd), yprev(dd), wsum(dd), besty(dd), claimy(dd), ywin(dd),
