@@ -95,3 +95,17 @@ def test_bad_arguments_rejected(emu_engine):
     with pytest.raises(nat.NativeError):
         dev.handle.ftp(args)
     dev.close()
+
+
+def test_integration_doc_binding_matches_header():
+    """The ctypes structs a reference maintainer would copy from INTEGRATION.md must have
+    exactly the fields of the package binding (itself checked against the header)."""
+    import re
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    block = doc[doc.index("class Problem(ctypes.Structure)"):doc.index("_lib.sc_create.argtypes")]
+    for cls, ours in (("Problem", nat.ScProblem), ("Args", nat.ScFtpArgs),
+                      ("Result", nat.ScFtpResult)):
+        body = block[block.index(f"class {cls}("):]
+        body = body[:body.index("]") + 1]
+        names = re.findall(r'\("(\w+)", ctypes\.c_\w+\)', body)
+        assert names == [f[0] for f in ours._fields_], cls
