@@ -62,3 +62,6 @@ inline int cuda_fail(sc_handle* h, cudaError_t e, const char* what) {
         cudaError_t _e = (call);                         \
         if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
     } while (0)
+
+// scmwu_gen.cu: draw a generated instance into the handle's X (and v1); *D_out = range
+int generate_rows(sc_handle* h, const sc_gen* gen, double* D_out);
