@@ -13,7 +13,6 @@ import pytest
 
 import oracle as O
 import parity as P
-from conftest import gf
 from paper_2405_09157_b200 import instances, meta, ses, svm
 
 pytestmark = pytest.mark.gpu

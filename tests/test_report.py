@@ -1,7 +1,6 @@
 """Run reports and sweeps (paper_2405_09157_b200.report, mirroring R/bench.py:22-161)."""
 import json
 
-import numpy as np
 import pytest
 
 from paper_2405_09157_b200 import RunConfig, report

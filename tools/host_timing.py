@@ -1,6 +1,5 @@
-import os, sys, time, ctypes
+import sys, time
 sys.path.insert(0, ".")
-import numpy as np
 import bench
 from paper_2405_09157_b200 import ses, _native as nat
 import torch
