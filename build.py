@@ -22,6 +22,7 @@ PKG = os.path.join(ROOT, "paper_2405_09157_b200")
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libscmwu.so")
+CHECKED_LIB = os.path.join(PKG, "libscmwu_checked.so")   # test-only (-DSCMWU_CHECKED)
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
@@ -49,28 +50,34 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_cuda(jobs: int | None = None, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build_cuda(jobs: int | None = None, force: bool = False, checked: bool = False) -> str:
+    """Compile csrc/*.cu into libscmwu.so.  ``checked``: the same sources with
+    -DSCMWU_CHECKED (device index invariants, SC_DCHECK) into libscmwu_checked.so, a
+    test-only library (tests/test_gpu_checked.py)."""
+    obj_dir = OBJ + "_checked" if checked else OBJ
+    lib = CHECKED_LIB if checked else LIB
+    flags = NVFLAGS + (["-DSCMWU_CHECKED"] if checked else [])
+    os.makedirs(obj_dir, exist_ok=True)
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "scmwu.h")]
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     objs = []
     todo = []
     for s in srcs:
-        o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
             todo.append((s, o))
 
     def compile_one(so):
         s, o = so
-        _run([NVCC] + NVFLAGS + ["-c", s, "-o", o], log=o + ".log")
+        _run([NVCC] + flags + ["-c", s, "-o", o], log=o + ".log")
 
     with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
         list(ex.map(compile_one, todo))
-    if force or todo or _stale(LIB, objs):
-        _run([NVCC, "-shared"] + ARCH + ["-o", LIB] + objs + ["-lcudart"])
-    return LIB
+    if force or todo or _stale(lib, objs):
+        _run([NVCC, "-shared"] + ARCH + ["-o", lib] + objs + ["-lcudart"])
+    return lib
 
 
 def build_oracle() -> None:
@@ -90,12 +97,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--emu", action="store_true")
     ap.add_argument("--force", action="store_true")
+    ap.add_argument("--checked", action="store_true", help="also build libscmwu_checked.so")
     ap.add_argument("-j", type=int, default=None)
     a = ap.parse_args()
     build_oracle()
     if a.emu:
         build_emu()
     print(build_cuda(a.j, a.force))
+    if a.checked:
+        print(build_cuda(a.j, a.force, checked=True))
 
 
 if __name__ == "__main__":

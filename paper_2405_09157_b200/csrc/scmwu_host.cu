@@ -273,11 +273,17 @@ static int configure(sc_handle* h, int grid_req) {
         }
     }
     int nwt = 0;
+    int64_t covered = 0;   // rows over all slots' tiles: must be n exactly (no gap, no overlap)
     for (int sl = 0; sl < G; ++sl) {
         const int64_t c0 = cta[4 * sl], c1 = cta[4 * sl + 1], st = cta[4 * sl + 2];
         const int t = c1 > c0 && st > 0 ? (int)((c1 - c0 + st - 1) / st) : 0;
         nwt = std::max(nwt, t);
+        if (t > 0) {
+            if (c0 < 0 || c1 > n || st < tr) { h->err = "partition: bad slot range"; return SC_EARG; }
+            covered += (int64_t)(t - 1) * tr + std::min<int64_t>(tr, c1 - (c0 + (int64_t)(t - 1) * st));
+        }
     }
+    if (covered != n) { h->err = "partition does not cover the rows exactly once"; return SC_EARG; }
     const int per_warp = (nwt + kNW - 1) / kNW;
     auto need = [&](int sw) {
         return (size_t)kNW * sw * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, kNW * sw);

@@ -39,6 +39,25 @@
 
 #include "scmwu_control.h"
 
+// Index invariants of the streaming and reduction code, checked in -DSCMWU_CHECKED builds
+// (build.py --checked -> libscmwu_checked.so, tests/test_gpu_checked.py): a failed check
+// prints the condition and traps, which aborts the whole cooperative launch (no CTA is
+// left spinning in a grid barrier).  Compiled out of the product library.
+#ifdef SCMWU_CHECKED
+#define SC_DCHECK(c)                                                                       \
+    do {                                                                                   \
+        if (!(c)) {                                                                        \
+            printf("SC_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #c, (int)blockIdx.x, (int)threadIdx.x);                                 \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define SC_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 #pragma once
 
 namespace scmwu {
@@ -433,6 +452,9 @@ __device__ __forceinline__ void issue_tile(const KParams& p, const SmemMap& m, i
         rb = (b + 1) & ~(int64_t)1;
         bytes += (uint32_t)((rb - ra) * 8);
     }
+    SC_DCHECK(stage >= 0 && stage < p.stages && w >= 0 && w < kNW);
+    SC_DCHECK(a >= r0 && a < b && b <= r1 && r1 <= p.n && b - a <= p.tile_rows);
+    SC_DCHECK(xb <= p.rad_off && (p.kind != SC_SES || p.rad_off + (rb - ra) * 8 <= p.stage_stride));
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive_tx(&m.full[slot], bytes);
     if (ws.keep > 0) {   // the CTA's first `keep` tiles stay in L2 across passes
@@ -491,6 +513,7 @@ __device__ __forceinline__ const unsigned char* acquire_stage(const KParams& p,
                                                               const WarpStream& ws,
                                                               int pass_idx) {
     const int slot = w * p.stages + ws.s;
+    SC_DCHECK(ws.s >= 0 && ws.s < p.stages);
     if (!p.resident || pass_idx == 0) mbar_wait(&m.full[slot], ws.phase);
     return m.ring + (size_t)slot * p.stage_stride;
 }
@@ -974,8 +997,10 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         slot = (int)s;
     }
     // this slot's warp tiles: tile j covers rows [r0 + j * tstride, + tile_rows) below r1
+    SC_DCHECK(slot >= 0 && slot < p.G);
     const int64_t r0 = p.row_begin[4 * slot], r1 = p.row_begin[4 * slot + 1];
     const int64_t tstride = p.row_begin[4 * slot + 2];
+    SC_DCHECK(r0 >= 0 && r1 <= p.n && (r1 <= r0 || tstride >= p.tile_rows));
     const int nwt = r1 > r0 ? (int)((r1 - r0 + tstride - 1) / tstride) : 0;
     const bool isP = KIND == SC_SVM && p.row_begin[4 * slot + 3] != 0;
     if (threadIdx.x == 0) {
@@ -1100,6 +1125,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         // double-buffered by pass parity for the single-barrier redundant fold)
         double* const part = p.partials + (size_t)(pass_idx & 1) * p.G * p.rw;
         const int nw_act = nwt < kNW ? nwt : kNW;   // warps that own at least one tile
+        SC_DCHECK(KIND != SC_SES || p.rw <= pws);
         for (int j = tid; j < p.rw; j += kNW * 32) {
             double v;
             if (KIND == SC_SES) {
@@ -1177,6 +1203,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             // column-distributed fold over this rank's G partials: warp per column, fixed
             // tree
             const double* gpart = part + (size_t)grp.first * p.rw;
+            SC_DCHECK(grp.G <= 160 && grp.first + grp.G <= p.G && c1 <= p.rw);
             for (int j = c0 + warp; j < c1; j += kNW) {
                 const int op = red_op(KIND, j);
                 double acc = op_identity(op);
@@ -1199,6 +1226,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
                         // mailbox (NVLink stores to the peers' HBM)
                         const size_t off =
                             ((size_t)((p.pass_base + pass_idx) & 1) * grp.W + grp.rank) * p.rw + j;
+                        SC_DCHECK(grp.W <= kMaxWorld && grp.rank < grp.W);
                         for (int r = 0; r < grp.W; ++r) p.mbox[r][off] = acc;
                         __threadfence_system();
                     } else {
