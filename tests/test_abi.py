@@ -43,6 +43,22 @@ def test_cuda_library_exports_every_symbol(cuda_lib_path):
     assert "sm_100a" in out.stdout, out.stdout[:500]
 
 
+def test_checked_library_exports_every_symbol(cuda_lib_path):
+    """libscmwu_checked.so (-DSCMWU_CHECKED, tests/test_gpu_checked.py) is the same ABI."""
+    import build
+    path = build.CHECKED_LIB
+    if not os.path.exists(path):
+        build.build_cuda(checked=True)
+    lib = ctypes.CDLL(path)
+    for sym in _declared():
+        assert hasattr(lib, sym), sym
+    # the checks are compiled into the checked library and out of the product library
+    with open(path, "rb") as fh:
+        assert b"SC_DCHECK failed" in fh.read()
+    with open(cuda_lib_path, "rb") as fh:
+        assert b"SC_DCHECK failed" not in fh.read()
+
+
 def test_emulator_exports_every_symbol(emu_engine):
     for sym in _declared():
         assert hasattr(emu_engine.lib, sym), sym
