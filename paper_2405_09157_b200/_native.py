@@ -187,6 +187,8 @@ class Engine:
                                 ctypes.byref(h))
         if st != SC_OK:
             msg = self.lib.sc_last_error(h).decode() if h.value else "sc_create failed"
+            if h.value:
+                self.lib.sc_destroy(h)
             if st == SC_ECUDA:
                 raise NativeUnavailable(f"CUDA engine cannot run: {msg}")
             raise NativeError(st, msg)

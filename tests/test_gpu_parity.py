@@ -269,3 +269,22 @@ def test_window_ring_overflow_fails_loudly(cuda_engine, monkeypatch):
     r = meta.refine_run(spec, D, 4000, meta.EarlyStopConfig(enabled=False), dev.progress)
     assert r.iterations == 4000
     dev.close()
+
+
+@pytest.mark.parametrize("kind", ["ses", "svm"])
+def test_rows_wider_than_512_rejected(cuda_engine, kind):
+    """d > 512 has no shared-memory layout yet: creation fails with SC_EARG
+    and a message instead of launching anything."""
+    from paper_2405_09157_b200 import _native as nat
+    if kind == "ses":
+        inst = instances.gen_ses(64, 513, 0, "gaussian")
+        with pytest.raises(nat.NativeError, match="d > 512"):
+            ses.ses_device(inst, engine=cuda_engine)
+    else:
+        inst, _ = instances.gen_svm(32, 32, 513, 0, 1.0)
+        with pytest.raises(nat.NativeError, match="d > 512"):
+            svm.svm_device(inst, engine=cuda_engine)
+    # the widest supported rows still work on the same engine
+    ok, _ = instances.gen_svm(40, 40, 512, 1, 1.0)
+    r, sol = svm.solve_svm(ok, 5e-2, engine=cuda_engine)
+    assert sol.margin > 0.0
