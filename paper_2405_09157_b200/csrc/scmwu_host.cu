@@ -189,6 +189,65 @@ static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb, bool full) {
 static std::mutex g_calib_mu;
 static std::map<std::pair<int, const void*>, std::vector<double>> g_calib;
 
+// The large per-handle buffers (X, radii, window ring) come from the device's
+// stream-ordered pool, which keeps up to SCMWU_POOL_GB (default 4) of freed memory mapped:
+// a solve through the public API creates and destroys a handle per call, and plain
+// cudaFree / cudaMalloc of ~1 GB cost 0.01-0.3 s each on B200 (C2: close 0.16-0.29 s,
+// ring growth up to 0.37 s, tools/solve_gaps.py).  Allocation and free are synchronised
+// on the handle's stream, so the memory is usable from any stream afterwards.  IPC-shared
+// mailboxes stay on cudaMalloc (pool memory cannot be exported with cudaIpcGetMemHandle).
+// Buffers larger than the retained size use plain cudaMalloc: the pool would release them
+// anyway, and growing it by 82 GB (C5 shape) took the e2e step (generate + 64 passes +
+// destroy) from 0.11 s to 0.40 s.
+static std::mutex g_pool_mu;
+static std::map<int, uint64_t> g_pool_thr;   // per device: retained bytes (set once)
+static std::map<void*, bool> g_pool_ptrs;    // live pointers that came from the pool
+
+static cudaError_t pool_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
+    uint64_t thr;
+    {
+        std::lock_guard<std::mutex> lock(g_pool_mu);
+        auto it = g_pool_thr.find(device);
+        if (it == g_pool_thr.end()) {
+            double gb = 4.0;
+            if (const char* e = getenv("SCMWU_POOL_GB")) gb = std::max(0.0, atof(e));
+            thr = (uint64_t)(gb * 1073741824.0);
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess ||
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) !=
+                    cudaSuccess)
+                thr = 0;
+            cudaGetLastError();
+            g_pool_thr[device] = thr;
+        } else {
+            thr = it->second;
+        }
+    }
+    if (bytes > thr) return cudaMalloc(p, bytes);
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lock(g_pool_mu);
+        g_pool_ptrs[*p] = true;
+    }
+    return cudaStreamSynchronize(s);
+}
+
+static void pool_free(void* p, cudaStream_t s) {
+    if (p == nullptr) return;
+    bool pooled;
+    {
+        std::lock_guard<std::mutex> lock(g_pool_mu);
+        pooled = g_pool_ptrs.erase(p) > 0;
+    }
+    if (!pooled) {
+        cudaFree(p);
+        return;
+    }
+    cudaFreeAsync(p, s);
+    cudaStreamSynchronize(s);
+}
+
 static bool balance_enabled() {
     const char* e = getenv("SCMWU_BALANCE");
     return e == nullptr || atoi(e) != 0;
@@ -464,7 +523,7 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
     CK(cudaEventCreate(&h->mk1), "event");
     // X: n x ld, rows padded to an even length (16-byte rows for the bulk copies)
     const size_t xbytes = (size_t)n * h->ld * sizeof(double);
-    CK(cudaMalloc(&h->X, xbytes), "alloc X");
+    CK(pool_alloc((void**)&h->X, xbytes, prob->device, h->stream), "alloc X");
     const int64_t n_head = X_tail ? prob->n1 : n;
     CK(cudaMalloc(&h->v1, (size_t)d * 8), "alloc anchor");
     CK(cudaMemset(h->v1, 0, (size_t)d * 8), "zero anchor");
@@ -481,7 +540,7 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
     }
     if (prob->kind == SC_SES) {
         const int64_t nr = (n + 1) & ~(int64_t)1;
-        CK(cudaMalloc(&h->radii, (size_t)(nr + 2) * 8), "alloc radii");
+        CK(pool_alloc((void**)&h->radii, (size_t)(nr + 2) * 8, prob->device, h->stream), "alloc radii");
         CK(cudaMemset(h->radii, 0, (size_t)(nr + 2) * 8), "zero radii");
         if (radii) {
             CK(cudaMemcpy(h->radii, radii, (size_t)n * 8, cudaMemcpyHostToDevice), "copy radii");
@@ -665,9 +724,10 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     const int64_t cap_lim = std::max<int64_t>(kLadderBase + 2, (int64_t)(ring_gb * 1073741824.0) / (dd8 * 8));
     if (need > cap_lim) need = cap_lim;
     if (need > h->ring_cap) {
-        if (h->ring) cudaFree(h->ring);
+        pool_free(h->ring, h->stream);
         h->ring = nullptr;
-        CK(cudaMalloc(&h->ring, (size_t)need * dd8 * 8), "alloc window ring");
+        CK(pool_alloc((void**)&h->ring, (size_t)need * dd8 * 8, h->prob.device, h->stream),
+           "alloc window ring");
         h->ring_cap = need;
     }
     KParams p;
@@ -1064,6 +1124,12 @@ const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "nul
 void sc_destroy(sc_handle* h) {
     if (!h) return;
     cudaSetDevice(h->prob.device);
+    if (h->stream) {   // pool buffers (see pool_alloc)
+        pool_free(h->X, h->stream);
+        pool_free(h->radii, h->stream);
+        pool_free(h->ring, h->stream);
+        h->X = nullptr; h->radii = nullptr; h->ring = nullptr;
+    }
     void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar, h->timing,
                     h->ring, h->slots, h->res, h->y_tilde, h->best_y, h->scratch, h->yvec,
                     h->status, h->v1, h->mbox_base};

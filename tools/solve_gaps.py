@@ -1,0 +1,59 @@
+"""Where the non-kernel wall time of one C2 solve goes (dev tool): every native call
+made by solve_ses (sc_ftp, sc_progress, ...) is timed on the host; prints per call
+wall vs kernel time and the host gaps between calls.
+
+    python tools/solve_gaps.py [--reps 3] [--resident]
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2405_09157_b200 import ses, _native as nat  # noqa: E402
+
+LOG = []
+
+
+def wrap(name):
+    fn = getattr(nat.Handle, name)
+
+    def timed(self, *a, **k):
+        t0 = time.perf_counter()
+        out = fn(self, *a, **k)
+        t1 = time.perf_counter()
+        LOG.append((name, t0, t1, getattr(out, "kernel_ms", 0.0) / 1e3,
+                    getattr(out, "passes", 0)))
+        return out
+    setattr(nat.Handle, name, timed)
+
+
+def main():
+    reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
+    for name in ("ftp", "progress", "iterate", "pd_pair", "close", "set_range"):
+        wrap(name)
+    w = bench.WORKLOADS["ses_c2"]
+    inst = bench.make_instance(w, pinned=True)
+    dev = ses.ses_device(inst) if "--resident" in sys.argv else None
+    for rep in range(reps):
+        LOG.clear()
+        t0 = time.perf_counter()
+        r, _ = ses.solve_ses(inst, w["eps"], device=dev)
+        t1 = time.perf_counter()
+        calls = sum(c[2] - c[1] for c in LOG)
+        kern = sum(c[3] for c in LOG)
+        gaps = [(LOG[i][1] - LOG[i - 1][2], LOG[i - 1][0], LOG[i][0]) for i in range(1, len(LOG))]
+        gaps.sort(reverse=True)
+        first = LOG[0][1] - t0 if LOG else 0.0
+        print(f"rep {rep}: total {t1 - t0:.3f}s  native calls {len(LOG)} wall {calls:.3f}s "
+              f"(ftp kernel {kern:.3f}s)  before first call {first:.3f}s  "
+              f"host gaps {sum(g[0] for g in gaps):.3f}s", flush=True)
+        slow = sorted(LOG, key=lambda c: (c[2] - c[1]) - c[3], reverse=True)[:5]
+        for c in slow:
+            print(f"   {c[0]:9s} wall {c[2] - c[1]:.4f}s kernel {c[3]:.4f}s passes {c[4]}")
+        for g in gaps[:3]:
+            print(f"   gap {g[0]:.4f}s  {g[1]} -> {g[2]}")
+
+
+if __name__ == "__main__":
+    main()
