@@ -189,8 +189,8 @@ static KernelFn kernel_lookup(int kind, int lpr, int cpl, int nb, bool full) {
 static std::mutex g_calib_mu;
 static std::map<std::pair<int, const void*>, std::vector<double>> g_calib;
 
-// The large per-handle buffers (X, radii, window ring) come from the device's
-// stream-ordered pool, which keeps up to SCMWU_POOL_GB (default 4) of freed memory mapped:
+// The per-handle device buffers (X, radii, window ring, partials, control slots, ...) come
+// from the device's stream-ordered pool, which keeps up to SCMWU_POOL_GB (default 4) of freed memory mapped:
 // a solve through the public API creates and destroys a handle per call, and plain
 // cudaFree / cudaMalloc of ~1 GB cost 0.01-0.3 s each on B200 (C2: close 0.16-0.29 s,
 // ring growth up to 0.37 s, tools/solve_gaps.py).  Allocation and free are synchronised
@@ -395,12 +395,12 @@ static int configure(sc_handle* h, int grid_req) {
     if (h->smem > (size_t)kMaxSmem) { h->err = "shared memory budget exceeded"; return SC_EARG; }
     h->grid = G;
     h->cta_h = cta;
-    if (h->row_begin) cudaFree(h->row_begin);
-    if (h->partials) cudaFree(h->partials);
-    CK(cudaMalloc(&h->row_begin, cta.size() * sizeof(int64_t)), "alloc rows");
+    pool_free(h->row_begin, h->stream);
+    pool_free(h->partials, h->stream);
+    CK(pool_alloc((void**)&h->row_begin, cta.size() * sizeof(int64_t), h->prob.device, h->stream), "alloc rows");
     CK(cudaMemcpy(h->row_begin, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
        "copy rows");
-    CK(cudaMalloc(&h->partials, 2 * (size_t)G * h->rw * sizeof(double)), "alloc partials");
+    CK(pool_alloc((void**)&h->partials, 2 * (size_t)G * h->rw * sizeof(double), h->prob.device, h->stream), "alloc partials");
     CK(cudaFuncSetAttribute(h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem),
        "smem attribute");
     int per_sm = 0;
@@ -525,7 +525,7 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
     const size_t xbytes = (size_t)n * h->ld * sizeof(double);
     CK(pool_alloc((void**)&h->X, xbytes, prob->device, h->stream), "alloc X");
     const int64_t n_head = X_tail ? prob->n1 : n;
-    CK(cudaMalloc(&h->v1, (size_t)d * 8), "alloc anchor");
+    CK(pool_alloc((void**)&h->v1, (size_t)d * 8, h->prob.device, h->stream), "alloc anchor");
     CK(cudaMemset(h->v1, 0, (size_t)d * 8), "zero anchor");
     if (gen) {
         const int st = generate_rows(h, gen, D_out);   // scmwu_gen.cu
@@ -616,18 +616,18 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
             for (int r = 0; r < W; ++r) h->peer_base[r] = static_cast<char*>(h->mbox_base) + mb * r;
         }
     }
-    CK(cudaMalloc(&h->red0, h->rw * 8), "alloc red0");
+    CK(pool_alloc((void**)&h->red0, h->rw * 8, h->prob.device, h->stream), "alloc red0");
     CK(cudaMemcpy(h->red0, h->red0_h.data(), h->rw * 8, cudaMemcpyHostToDevice), "copy red0");
-    CK(cudaMalloc(&h->redg, h->rw * 8), "alloc redg");
-    CK(cudaMalloc(&h->bar, 1024), "alloc barrier");   // + one counter per emulated rank
-    CK(cudaMalloc(&h->slots, (size_t)kNumSlots * h->slot_len * 8), "alloc slots");
+    CK(pool_alloc((void**)&h->redg, h->rw * 8, h->prob.device, h->stream), "alloc redg");
+    CK(pool_alloc((void**)&h->bar, 1024, h->prob.device, h->stream), "alloc barrier");   // + one counter per emulated rank
+    CK(pool_alloc((void**)&h->slots, (size_t)kNumSlots * h->slot_len * 8, h->prob.device, h->stream), "alloc slots");
     CK(cudaMemset(h->slots, 0, (size_t)kNumSlots * h->slot_len * 8), "zero slots");
-    CK(cudaMalloc(&h->res, sizeof(sc_ftp_result)), "alloc result");
-    CK(cudaMalloc(&h->y_tilde, h->dd * 8), "alloc y");
-    CK(cudaMalloc(&h->best_y, h->dd * 8), "alloc y");
-    CK(cudaMalloc(&h->yvec, (size_t)(d + 2) * 8), "alloc y");
-    CK(cudaMalloc(&h->status, sizeof(int)), "alloc status");
-    CK(cudaMalloc(&h->scratch, 2 * 4096 * 8), "alloc scratch");
+    CK(pool_alloc((void**)&h->res, sizeof(sc_ftp_result), h->prob.device, h->stream), "alloc result");
+    CK(pool_alloc((void**)&h->y_tilde, h->dd * 8, h->prob.device, h->stream), "alloc y");
+    CK(pool_alloc((void**)&h->best_y, h->dd * 8, h->prob.device, h->stream), "alloc y");
+    CK(pool_alloc((void**)&h->yvec, (size_t)(d + 2) * 8, h->prob.device, h->stream), "alloc y");
+    CK(pool_alloc((void**)&h->status, sizeof(int), h->prob.device, h->stream), "alloc status");
+    CK(pool_alloc((void**)&h->scratch, 2 * 4096 * 8, h->prob.device, h->stream), "alloc scratch");
     int st = configure(h, prob->grid);
     if (st != SC_OK) return st;
     h->err.clear();
@@ -1124,19 +1124,13 @@ const char* sc_last_error(const sc_handle* h) { return h ? h->err.c_str() : "nul
 void sc_destroy(sc_handle* h) {
     if (!h) return;
     cudaSetDevice(h->prob.device);
-    if (h->stream) {   // pool buffers (see pool_alloc)
-        pool_free(h->X, h->stream);
-        pool_free(h->radii, h->stream);
-        pool_free(h->ring, h->stream);
-        h->X = nullptr; h->radii = nullptr; h->ring = nullptr;
-    }
     void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar, h->timing,
                     h->ring, h->slots, h->res, h->y_tilde, h->best_y, h->scratch, h->yvec,
                     h->status, h->v1, h->mbox_base};
     for (int r = 0; r < kMaxWorld && h->vworld <= 1; ++r)   // emulated ranks: own memory
         if (h->peer_base[r] && h->peer_base[r] != h->mbox_base) cudaIpcCloseMemHandle(h->peer_base[r]);
-    for (void* b : bufs)
-        if (b) cudaFree(b);
+    for (void* b : bufs)   // pool or cudaMalloc memory (pool_free tells them apart)
+        if (b) { if (h->stream) pool_free(b, h->stream); else cudaFree(b); }
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->mk0) cudaEventDestroy(h->mk0);

@@ -32,6 +32,22 @@ def main():
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
     for name in ("ftp", "progress", "iterate", "pd_pair", "close", "set_range"):
         wrap(name)
+    create = nat.Engine.create
+
+    def timed_create(self, *a, **k):
+        t0 = time.perf_counter()
+        out = create(self, *a, **k)
+        LOG.append(("create", t0, time.perf_counter(), 0.0, 0))
+        return out
+    nat.Engine.create = timed_create
+    rng = ses.ses_range
+
+    def timed_range(*a, **k):
+        t0 = time.perf_counter()
+        out = rng(*a, **k)
+        LOG.append(("range", t0, time.perf_counter(), 0.0, 0))
+        return out
+    ses.ses_range = timed_range
     w = bench.WORKLOADS["ses_c2"]
     inst = bench.make_instance(w, pinned=True)
     dev = ses.ses_device(inst) if "--resident" in sys.argv else None
@@ -45,9 +61,11 @@ def main():
         gaps = [(LOG[i][1] - LOG[i - 1][2], LOG[i - 1][0], LOG[i][0]) for i in range(1, len(LOG))]
         gaps.sort(reverse=True)
         first = LOG[0][1] - t0 if LOG else 0.0
+        pre = {c[0]: c[2] - c[1] for c in LOG if c[0] in ("range", "create")}
         print(f"rep {rep}: total {t1 - t0:.3f}s  native calls {len(LOG)} wall {calls:.3f}s "
               f"(ftp kernel {kern:.3f}s)  before first call {first:.3f}s  "
-              f"host gaps {sum(g[0] for g in gaps):.3f}s", flush=True)
+              f"host gaps {sum(g[0] for g in gaps):.3f}s  "
+              + "  ".join(f"{k} {v:.3f}s" for k, v in pre.items()), flush=True)
         slow = sorted(LOG, key=lambda c: (c[2] - c[1]) - c[3], reverse=True)[:5]
         for c in slow:
             print(f"   {c[0]:9s} wall {c[2] - c[1]:.4f}s kernel {c[3]:.4f}s passes {c[4]}")
