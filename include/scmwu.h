@@ -208,6 +208,10 @@ int sc_info(const sc_handle* h, int64_t* out /* 8 values: grid, threads, lanes_p
 const char* sc_last_error(const sc_handle* h);
 void sc_destroy(sc_handle* h);
 int sc_version(void);
+/* Release the device memory the engine's private pool keeps mapped for reuse (freed
+ * buffers up to SCMWU_POOL_GB, default 12 GiB, stay mapped so a solve per call through the
+ * public API does not pay cudaMalloc / cudaFree of the matrix every time). */
+int sc_pool_trim(int32_t device);
 
 #ifdef __cplusplus
 }

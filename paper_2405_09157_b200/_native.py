@@ -81,7 +81,8 @@ EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "
            "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_debug_timing",
            "sc_local_red0", "sc_progress_parts", "sc_set_globals", "sc_ipc_handle",
            "sc_connect", "sc_last_error", "sc_destroy", "sc_version", "sc_create_generated",
-           "sc_set_range", "sc_read_rows", "sc_meb_baseline", "sc_gilbert_baseline")
+           "sc_set_range", "sc_read_rows", "sc_meb_baseline", "sc_gilbert_baseline",
+           "sc_pool_trim")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -117,6 +118,7 @@ class Engine:
         lib.sc_destroy.argtypes = [vp]
         lib.sc_destroy.restype = None
         lib.sc_version.restype = ctypes.c_int
+        lib.sc_pool_trim.argtypes = [ctypes.c_int32]
         lib.sc_mark.argtypes = [vp, ctypes.c_int32]
         lib.sc_elapsed.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
         lib.sc_launches.argtypes = [vp]
@@ -135,6 +137,13 @@ class Engine:
         lib.sc_gilbert_baseline.argtypes = [vp, ctypes.c_double, ctypes.c_int64, _dp, _dp,
                                             ctypes.POINTER(ctypes.c_int64), _dp, _dp]
         self.lib = lib
+
+    def trim_pool(self, device: int = 0) -> None:
+        """Return the device memory the engine's private pool keeps for reuse
+        (sc_pool_trim)."""
+        st = self.lib.sc_pool_trim(device)
+        if st != SC_OK:
+            raise RuntimeError(f"sc_pool_trim failed with status {st}")
 
     def create_generated(self, kind: int, n: int, d: int, seed: int, dist: int,
                          n1: int = 0, gap: float = 1.0, direction=None, grid: int = 0,

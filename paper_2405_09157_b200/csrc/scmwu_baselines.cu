@@ -220,9 +220,9 @@ int sc_meb_baseline(sc_handle* h, int64_t iters, double* center, double* value) 
     if (G < 1) { h->err = "baseline kernel does not fit"; return SC_ECUDA; }
     double *part = nullptr, *cout = nullptr;
     unsigned long long* bar = nullptr;
-    CK(cudaMalloc(&part, 4 * (size_t)G * 8), "alloc baseline");
-    CK(cudaMalloc(&cout, (size_t)d * 8), "alloc baseline");
-    CK(cudaMalloc(&bar, 8), "alloc baseline");
+    CK(pool_alloc((void**)&part, 4 * (size_t)G * 8, h->prob.device, h->stream), "alloc baseline");
+    CK(pool_alloc((void**)&cout, (size_t)d * 8, h->prob.device, h->stream), "alloc baseline");
+    CK(pool_alloc((void**)&bar, 8, h->prob.device, h->stream), "alloc baseline");
     CK(cudaMemsetAsync(bar, 0, 8, h->stream), "zero barrier");
     const double* X = h->X;
     const double* radii = h->radii;
@@ -236,10 +236,10 @@ int sc_meb_baseline(sc_handle* h, int64_t iters, double* center, double* value) 
                                                 h->stream);
     ++h->launches;
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    if (e == cudaSuccess) e = cudaMemcpy(center, cout, (size_t)d * 8, cudaMemcpyDeviceToHost);
-    cudaFree(part);
-    cudaFree(cout);
-    cudaFree(bar);
+    if (e == cudaSuccess) e = h_get(h, center, cout, (size_t)d * 8);
+    pool_free(part, h->stream);
+    pool_free(cout, h->stream);
+    pool_free(bar, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "meb baseline");
     if (value) return sc_progress(h, center, value);   // max_i |v_i - c| + r_i
     return SC_OK;
@@ -260,11 +260,11 @@ int sc_gilbert_baseline(sc_handle* h, double gap_tol, int64_t max_iters, double*
     if (G < 1) { h->err = "baseline kernel does not fit"; return SC_ECUDA; }
     double *part = nullptr, *zout = nullptr, *logb = nullptr, *info = nullptr;
     unsigned long long* bar = nullptr;
-    CK(cudaMalloc(&part, 8 * (size_t)G * 8), "alloc baseline");
-    CK(cudaMalloc(&zout, (size_t)d * 8), "alloc baseline");
-    CK(cudaMalloc(&logb, 3 * (size_t)std::max<int64_t>(1, max_iters) * 8), "alloc baseline log");
-    CK(cudaMalloc(&info, 4 * 8), "alloc baseline");
-    CK(cudaMalloc(&bar, 8), "alloc baseline");
+    CK(pool_alloc((void**)&part, 8 * (size_t)G * 8, h->prob.device, h->stream), "alloc baseline");
+    CK(pool_alloc((void**)&zout, (size_t)d * 8, h->prob.device, h->stream), "alloc baseline");
+    CK(pool_alloc((void**)&logb, 3 * (size_t)std::max<int64_t>(1, max_iters) * 8, h->prob.device, h->stream), "alloc baseline log");
+    CK(pool_alloc((void**)&info, 4 * 8, h->prob.device, h->stream), "alloc baseline");
+    CK(pool_alloc((void**)&bar, 8, h->prob.device, h->stream), "alloc baseline");
     CK(cudaMemsetAsync(bar, 0, 8, h->stream), "zero barrier");
     const double* X = h->X;
     double *pp = part, *zo = zout, *lg = logb, *inf = info;
@@ -279,17 +279,17 @@ int sc_gilbert_baseline(sc_handle* h, double gap_tol, int64_t max_iters, double*
     double hi[3] = {INFINITY, 0.0, 0.0};
     std::vector<double> z(d);
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
-    if (e == cudaSuccess) e = cudaMemcpy(hi, info, 3 * 8, cudaMemcpyDeviceToHost);
-    if (e == cudaSuccess) e = cudaMemcpy(z.data(), zout, (size_t)d * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = h_get(h, hi, info, 3 * 8);
+    if (e == cudaSuccess) e = h_get(h, z.data(), zout, (size_t)d * 8);
     const int64_t updates = (int64_t)hi[2];
     std::vector<double> lg_h(3 * (size_t)updates);
     if (e == cudaSuccess && updates > 0)
-        e = cudaMemcpy(lg_h.data(), logb, lg_h.size() * 8, cudaMemcpyDeviceToHost);
-    cudaFree(part);
-    cudaFree(zout);
-    cudaFree(logb);
-    cudaFree(info);
-    cudaFree(bar);
+        e = h_get(h, lg_h.data(), logb, lg_h.size() * 8);
+    pool_free(part, h->stream);
+    pool_free(zout, h->stream);
+    pool_free(logb, h->stream);
+    pool_free(info, h->stream);
+    pool_free(bar, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "gilbert baseline");
     if (max_iters == 0) { hi[1] = 0.0; }
     double nz = 0.0;

@@ -125,15 +125,14 @@ int generate_rows(sc_handle* h, const sc_gen* gen, double* D_out) {
     const int d = P.d;
     const int64_t n = P.n_local;
     // every rank draws the global anchor row 0 itself (SES), then its own rows
-    unsigned long long* dmax = nullptr;
+    // the handle's scratch (2 x 4096 doubles): the range word, then the SVM direction
+    unsigned long long* dmax = reinterpret_cast<unsigned long long*>(h->scratch);
     double* dir = nullptr;
-    CK(cudaMalloc(&dmax, 8), "alloc range");
     CK(cudaMemsetAsync(dmax, 0, 8, h->stream), "zero range");
     double shift = 0.0;
     if (prob->kind == SC_SVM) {
-        CK(cudaMalloc(&dir, (size_t)d * 8), "alloc direction");
-        CK(cudaMemcpy(dir, gen->direction, (size_t)d * 8, cudaMemcpyHostToDevice),
-           "copy direction");
+        dir = h->scratch + 8;
+        CK(h_put(h, dir, gen->direction, (size_t)d * 8), "copy direction");
         shift = 1.0 + gen->gap / 2.0;
     } else {
         gen_kernel<<<1, 32, 0, h->stream>>>(h->v1, d, d, 1, 0, gen->dist, gen->seed, P.n,
@@ -147,9 +146,7 @@ int generate_rows(sc_handle* h, const sc_gen* gen, double* D_out) {
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
     unsigned long long bits = 0;
-    if (e == cudaSuccess) e = cudaMemcpy(&bits, dmax, 8, cudaMemcpyDeviceToHost);
-    cudaFree(dmax);
-    if (dir) cudaFree(dir);
+    if (e == cudaSuccess) e = h_get(h, &bits, dmax, 8);
     if (e != cudaSuccess) return cuda_fail(h, e, "generate rows");
     memcpy(D_out, &bits, 8);
     return SC_OK;

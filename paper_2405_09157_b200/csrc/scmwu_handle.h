@@ -37,6 +37,8 @@ struct sc_handle {
     void* mbox_base = nullptr;
     void* peer_base[kMaxWorld] = {};
     bool connected = false;
+    bool pool_open = false;          // counted in the device pool's live handles
+    bool broken = false;             // a multi-GPU exchange failed: the handle is unusable
     int64_t pass_total = 0;          // passes of all previous calls (identical on all ranks)
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, mk0 = nullptr, mk1 = nullptr;
@@ -62,6 +64,29 @@ inline int cuda_fail(sc_handle* h, cudaError_t e, const char* what) {
         cudaError_t _e = (call);                         \
         if (_e != cudaSuccess) return cuda_fail(h, _e, what); \
     } while (0)
+
+// Every copy and memset of a handle's buffers is ordered on the handle's stream (plain
+// cudaMemset / cudaMemcpy would run on the legacy stream, which the handle's stream does
+// not wait for); the synchronous forms wait for the stream before returning.
+inline cudaError_t h_zero(sc_handle* h, void* p, size_t bytes) {
+    return cudaMemsetAsync(p, 0, bytes, h->stream);
+}
+inline cudaError_t h_copy(sc_handle* h, void* dst, const void* src, size_t bytes,
+                          cudaMemcpyKind kind) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, h->stream);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(h->stream);
+}
+inline cudaError_t h_put(sc_handle* h, void* dst, const void* src, size_t bytes) {
+    return h_copy(h, dst, src, bytes, cudaMemcpyHostToDevice);
+}
+inline cudaError_t h_get(sc_handle* h, void* dst, const void* src, size_t bytes) {
+    return h_copy(h, dst, src, bytes, cudaMemcpyDeviceToHost);
+}
+
+// scmwu_host.cu: the engine's private stream-ordered pool (freed memory up to SCMWU_POOL_GB
+// stays mapped while a handle of the device is alive); larger buffers use cudaMalloc
+cudaError_t pool_alloc(void** p, size_t bytes, int device, cudaStream_t s);
+void pool_free(void* p, cudaStream_t s);
 
 // scmwu_gen.cu: draw a generated instance into the handle's X (and v1); *D_out = range
 int generate_rows(sc_handle* h, const sc_gen* gen, double* D_out);

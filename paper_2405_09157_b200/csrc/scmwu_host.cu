@@ -136,13 +136,13 @@ static cudaError_t column_sums(sc_handle* h, int64_t a, int64_t b, double* out) 
     const int d = h->prob.d;
     const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (b - a) / 256));
     double* part = nullptr;
-    cudaError_t e = cudaMalloc(&part, (size_t)chunks * d * 8);
+    cudaError_t e = pool_alloc((void**)&part, (size_t)chunks * d * 8, h->prob.device, h->stream);
     if (e != cudaSuccess) return e;
     colsum_chunk_kernel<<<dim3((d + 31) / 32, chunks), 256, 0, h->stream>>>(h->X, a, b, d, h->ld,
                                                                           chunks, part);
     colsum_fold_kernel<<<(d + 127) / 128, 128, 0, h->stream>>>(part, chunks, d, out);
     e = cudaStreamSynchronize(h->stream);
-    cudaFree(part);
+    pool_free(part, h->stream);
     return e;
 }
 
@@ -200,31 +200,46 @@ static std::map<std::pair<int, const void*>, std::vector<double>> g_calib;
 // anyway, and growing it by 82 GB (C5 shape) took the e2e step (generate + 64 passes +
 // destroy) from 0.11 s to 0.40 s.
 static std::mutex g_pool_mu;
-static std::map<int, uint64_t> g_pool_thr;   // per device: retained bytes (set once)
+struct DevPool {
+    cudaMemPool_t pool = nullptr;   // private to the engine (not the device's default pool)
+    uint64_t thr = 0;               // retained bytes
+    int handles = 0;                // live handles on the device
+};
+static std::map<int, DevPool> g_pools;
 static std::map<void*, bool> g_pool_ptrs;    // live pointers that came from the pool
 
-static cudaError_t pool_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
-    uint64_t thr;
+static DevPool& dev_pool(int device) {   // g_pool_mu held
+    auto it = g_pools.find(device);
+    if (it != g_pools.end()) return it->second;
+    DevPool& dp = g_pools[device];
+    double gb = 12.0;   // >= the C4 matrix (10^7 x 100 fp64 = 8 GB) plus its ring
+    if (const char* e = getenv("SCMWU_POOL_GB")) gb = std::max(0.0, atof(e));
+    dp.thr = (uint64_t)(gb * 1073741824.0);
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    if (dp.thr == 0 || cudaMemPoolCreate(&dp.pool, &props) != cudaSuccess ||
+        cudaMemPoolSetAttribute(dp.pool, cudaMemPoolAttrReleaseThreshold, &dp.thr) !=
+            cudaSuccess) {
+        dp.pool = nullptr;
+        dp.thr = 0;
+    }
+    cudaGetLastError();
+    return dp;
+}
+
+cudaError_t pool_alloc(void** p, size_t bytes, int device, cudaStream_t s) {
+    cudaMemPool_t pool;
     {
         std::lock_guard<std::mutex> lock(g_pool_mu);
-        auto it = g_pool_thr.find(device);
-        if (it == g_pool_thr.end()) {
-            double gb = 4.0;
-            if (const char* e = getenv("SCMWU_POOL_GB")) gb = std::max(0.0, atof(e));
-            thr = (uint64_t)(gb * 1073741824.0);
-            cudaMemPool_t pool;
-            if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess ||
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) !=
-                    cudaSuccess)
-                thr = 0;
-            cudaGetLastError();
-            g_pool_thr[device] = thr;
-        } else {
-            thr = it->second;
-        }
+        DevPool& dp = dev_pool(device);
+        pool = bytes <= dp.thr ? dp.pool : nullptr;
     }
-    if (bytes > thr) return cudaMalloc(p, bytes);
-    cudaError_t e = cudaMallocAsync(p, bytes, s);
+    if (pool == nullptr) return cudaMalloc(p, std::max<size_t>(bytes, 8));
+    cudaError_t e = cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 8), pool, s);
     if (e != cudaSuccess) return e;
     {
         std::lock_guard<std::mutex> lock(g_pool_mu);
@@ -233,7 +248,7 @@ static cudaError_t pool_alloc(void** p, size_t bytes, int device, cudaStream_t s
     return cudaStreamSynchronize(s);
 }
 
-static void pool_free(void* p, cudaStream_t s) {
+void pool_free(void* p, cudaStream_t s) {
     if (p == nullptr) return;
     bool pooled;
     {
@@ -246,6 +261,20 @@ static void pool_free(void* p, cudaStream_t s) {
     }
     cudaFreeAsync(p, s);
     cudaStreamSynchronize(s);
+}
+
+// live handles per device.  The pool keeps freed memory mapped after the last handle
+// closes (a public-API solve creates and destroys a handle per call); sc_pool_trim returns
+// it to the driver.  The pool is private to the engine, so no other cudaMallocAsync user of
+// the process (torch, NCCL) inherits the retention threshold.
+static void pool_handle_open(int device) {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    dev_pool(device).handles += 1;
+}
+static void pool_handle_close(int device) {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    DevPool& dp = dev_pool(device);
+    if (dp.handles > 0) dp.handles -= 1;
 }
 
 static bool balance_enabled() {
@@ -398,7 +427,7 @@ static int configure(sc_handle* h, int grid_req) {
     pool_free(h->row_begin, h->stream);
     pool_free(h->partials, h->stream);
     CK(pool_alloc((void**)&h->row_begin, cta.size() * sizeof(int64_t), h->prob.device, h->stream), "alloc rows");
-    CK(cudaMemcpy(h->row_begin, cta.data(), cta.size() * sizeof(int64_t), cudaMemcpyHostToDevice),
+    CK(h_put(h, h->row_begin, cta.data(), cta.size() * sizeof(int64_t)),
        "copy rows");
     CK(pool_alloc((void**)&h->partials, 2 * (size_t)G * h->rw * sizeof(double), h->prob.device, h->stream), "alloc partials");
     CK(cudaFuncSetAttribute(h->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem),
@@ -462,6 +491,13 @@ extern "C" {
 
 int sc_version(void) { return 1000; }
 
+int sc_pool_trim(int32_t device) {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    auto it = g_pools.find(device);
+    if (it == g_pools.end() || it->second.pool == nullptr) return SC_OK;
+    return cudaMemPoolTrimTo(it->second.pool, 0) == cudaSuccess ? SC_OK : SC_ECUDA;
+}
+
 // sc_create (host rows X / X_tail / radii) and sc_create_generated (gen != NULL: rows drawn
 // on the device, zero radii; *D_out receives this shard's range D)
 static int create_impl(const sc_problem* prob, const double* X, const double* X_tail,
@@ -517,6 +553,8 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
     if (!dp.cooperativeLaunch) { h->err = "cooperative launch unsupported"; return SC_ECUDA; }
     h->sms = dp.multiProcessorCount;
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "stream");
+    pool_handle_open(prob->device);
+    h->pool_open = true;
     CK(cudaEventCreate(&h->ev0), "event");
     CK(cudaEventCreate(&h->ev1), "event");
     CK(cudaEventCreate(&h->mk0), "event");
@@ -524,26 +562,27 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
     // X: n x ld, rows padded to an even length (16-byte rows for the bulk copies)
     const size_t xbytes = (size_t)n * h->ld * sizeof(double);
     CK(pool_alloc((void**)&h->X, xbytes, prob->device, h->stream), "alloc X");
+    CK(pool_alloc((void**)&h->scratch, 2 * 4096 * 8, h->prob.device, h->stream), "alloc scratch");
     const int64_t n_head = X_tail ? prob->n1 : n;
     CK(pool_alloc((void**)&h->v1, (size_t)d * 8, h->prob.device, h->stream), "alloc anchor");
-    CK(cudaMemset(h->v1, 0, (size_t)d * 8), "zero anchor");
+    CK(h_zero(h, h->v1, (size_t)d * 8), "zero anchor");
     if (gen) {
         const int st = generate_rows(h, gen, D_out);   // scmwu_gen.cu
         if (st != SC_OK) return st;
     } else {
-        if (h->ld != d) CK(cudaMemset(h->X, 0, xbytes), "zero X");
+        if (h->ld != d) CK(h_zero(h, h->X, xbytes), "zero X");   // ordered before the upload
         int up = upload_rows(h, h->X, X, n_head, d);
         if (up == SC_OK && X_tail) up = upload_rows(h, h->X + n_head * h->ld, X_tail, n - n_head, d);
         if (up != SC_OK) return up;
         // SES anchor row (global row 0; sharded: sc_set_globals provides it)
-        if (P.row0 == 0) CK(cudaMemcpy(h->v1, X, (size_t)d * 8, cudaMemcpyHostToDevice), "anchor");
+        if (P.row0 == 0) CK(h_put(h, h->v1, X, (size_t)d * 8), "anchor");
     }
     if (prob->kind == SC_SES) {
         const int64_t nr = (n + 1) & ~(int64_t)1;
         CK(pool_alloc((void**)&h->radii, (size_t)(nr + 2) * 8, prob->device, h->stream), "alloc radii");
-        CK(cudaMemset(h->radii, 0, (size_t)(nr + 2) * 8), "zero radii");
+        CK(h_zero(h, h->radii, (size_t)(nr + 2) * 8), "zero radii");
         if (radii) {
-            CK(cudaMemcpy(h->radii, radii, (size_t)n * 8, cudaMemcpyHostToDevice), "copy radii");
+            CK(h_put(h, h->radii, radii, (size_t)n * 8), "copy radii");
             h->g1 = P.row0 == 0 ? radii[0] : 0.0;   // sharded: sc_set_globals provides it
         }
     }
@@ -561,14 +600,12 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
         const int64_t n1l = P.n1_local;
         h->red0_h[kV_TP] = (double)n1l;
         h->red0_h[kV_TQ] = (double)(n - n1l);
-        double* cs = nullptr;
-        CK(cudaMalloc(&cs, 2 * (size_t)d * 8), "alloc colsum");
+        double* cs = h->scratch;   // 2 x 4096 doubles >= 2 d
         CK(column_sums(h, 0, n1l, cs), "colsum P");
         CK(column_sums(h, n1l, n, cs + d), "colsum Q");
         h->launches += 4;
-        CK(cudaMemcpy(h->red0_h.data() + kV_Vec, cs, 2 * (size_t)d * 8, cudaMemcpyDeviceToHost),
+        CK(h_get(h, h->red0_h.data() + kV_Vec, cs, 2 * (size_t)d * 8),
            "copy colsum");
-        cudaFree(cs);
     }
     // Emulated ranks on one GPU (tests only, SCMWU_VWORLD = 2..8 with world <= 1): the
     // iterate-1 vector is the rank-ordered fold of the ranks' local vectors, exactly as a
@@ -583,8 +620,7 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
                 const int op = red_op(prob->kind, j);
                 acc[j] = op_identity(op);
             }
-            double* cs = nullptr;
-            CK(cudaMalloc(&cs, 2 * (size_t)d * 8), "alloc colsum");
+            double* cs = h->scratch;
             for (int r = 0; r < W; ++r) {
                 const int64_t q = n / W, m = n % W;
                 const int64_t R0 = r * q + std::min<int64_t>(r, m), R1 = R0 + q + (r < m ? 1 : 0);
@@ -602,32 +638,30 @@ static int create_impl(const sc_problem* prob, const double* X, const double* X_
                     loc[kV_TQ] = (double)(R1 - p1);
                     CK(column_sums(h, R0, p1, cs), "colsum P");
                     CK(column_sums(h, p1, R1, cs + d), "colsum Q");
-                    CK(cudaMemcpy(loc.data() + kV_Vec, cs, 2 * (size_t)d * 8,
-                                  cudaMemcpyDeviceToHost), "copy colsum");
+                    CK(h_get(h, loc.data() + kV_Vec, cs, 2 * (size_t)d * 8), "copy colsum");
                 }
                 for (int j = 0; j < h->rw; ++j) acc[j] = op_apply(red_op(prob->kind, j), acc[j], loc[j]);
             }
-            cudaFree(cs);
             h->red0_h = acc;
             // mailboxes of all emulated ranks: [flags 64 | data 2 x W x rw] each
             const size_t mb = 64 * 8 + 2 * (size_t)W * h->rw * 8;
             CK(cudaMalloc(&h->mbox_base, mb * W), "alloc mailboxes");
-            CK(cudaMemset(h->mbox_base, 0, mb * W), "zero mailboxes");
+            CK(h_zero(h, h->mbox_base, mb * W), "zero mailboxes");
+            CK(cudaStreamSynchronize(h->stream), "zero mailboxes");
             for (int r = 0; r < W; ++r) h->peer_base[r] = static_cast<char*>(h->mbox_base) + mb * r;
         }
     }
     CK(pool_alloc((void**)&h->red0, h->rw * 8, h->prob.device, h->stream), "alloc red0");
-    CK(cudaMemcpy(h->red0, h->red0_h.data(), h->rw * 8, cudaMemcpyHostToDevice), "copy red0");
+    CK(h_put(h, h->red0, h->red0_h.data(), h->rw * 8), "copy red0");
     CK(pool_alloc((void**)&h->redg, h->rw * 8, h->prob.device, h->stream), "alloc redg");
     CK(pool_alloc((void**)&h->bar, 1024, h->prob.device, h->stream), "alloc barrier");   // + one counter per emulated rank
     CK(pool_alloc((void**)&h->slots, (size_t)kNumSlots * h->slot_len * 8, h->prob.device, h->stream), "alloc slots");
-    CK(cudaMemset(h->slots, 0, (size_t)kNumSlots * h->slot_len * 8), "zero slots");
+    CK(h_zero(h, h->slots, (size_t)kNumSlots * h->slot_len * 8), "zero slots");
     CK(pool_alloc((void**)&h->res, sizeof(sc_ftp_result), h->prob.device, h->stream), "alloc result");
     CK(pool_alloc((void**)&h->y_tilde, h->dd * 8, h->prob.device, h->stream), "alloc y");
     CK(pool_alloc((void**)&h->best_y, h->dd * 8, h->prob.device, h->stream), "alloc y");
     CK(pool_alloc((void**)&h->yvec, (size_t)(d + 2) * 8, h->prob.device, h->stream), "alloc y");
     CK(pool_alloc((void**)&h->status, sizeof(int), h->prob.device, h->stream), "alloc status");
-    CK(pool_alloc((void**)&h->scratch, 2 * 4096 * 8, h->prob.device, h->stream), "alloc scratch");
     int st = configure(h, prob->grid);
     if (st != SC_OK) return st;
     h->err.clear();
@@ -676,7 +710,7 @@ int sc_create_generated(sc_problem* prob, const sc_gen* gen, double* v1_out, sc_
     h->prob.rank = prob->rank;
     h->prob.ln_r = prob->ln_r;
     if (v1_out && prob->kind == SC_SES)
-        CK(cudaMemcpy(v1_out, h->v1, (size_t)prob->d * 8, cudaMemcpyDeviceToHost), "copy anchor");
+        CK(h_get(h, v1_out, h->v1, (size_t)prob->d * 8), "copy anchor");
     return SC_OK;
 }
 
@@ -706,6 +740,10 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
                     double* y_tilde, double* best_y, long long* slot_cycles) {
     if (!h || !args || !res || !y_tilde || !best_y) return SC_EARG;
     memset(res, 0, sizeof(*res));
+    if (h->broken) {
+        h->err = "handle unusable after a multi-GPU exchange failure";
+        return SC_ENCCL;
+    }
     if (args->mode != SC_MODE_FTP && args->mode != SC_MODE_REFINE) return SC_EARG;
     if (!(args->alpha > 0.0)) { h->err = "alpha must be positive"; return SC_EARG; }
     const int64_t T = args->mode == SC_MODE_FTP ? args->budget : args->horizon;
@@ -775,6 +813,13 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     p.row0 = h->prob.row0;
     p.pass_base = h->pass_total;
     p.vworld = h->vworld;
+    {   // peer timeout of the in-kernel exchange: SCMWU_EXCHANGE_TIMEOUT_S (default 30 s)
+        double secs = 30.0;
+        if (const char* e = getenv("SCMWU_EXCHANGE_TIMEOUT_S")) secs = std::max(1e-3, atof(e));
+        int khz = 0;
+        cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, h->prob.device);
+        p.xtimeout = (long long)(secs * 1e3 * (double)(khz > 0 ? khz : 2000000));
+    }
     if (h->vworld > 1) {
         for (int r = 0; r < h->vworld; ++r) {
             p.mflag[r] = reinterpret_cast<unsigned long long*>(h->peer_base[r]);
@@ -800,10 +845,10 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     CK(cudaEventRecord(h->ev1, h->stream), "event");
     CK(cudaStreamSynchronize(h->stream), "persistent kernel");
     int status = -1;
-    CK(cudaMemcpy(res, h->res, sizeof(sc_ftp_result), cudaMemcpyDeviceToHost), "copy result");
-    CK(cudaMemcpy(&status, h->status, sizeof(int), cudaMemcpyDeviceToHost), "copy status");
-    CK(cudaMemcpy(y_tilde, h->y_tilde, h->dd * 8, cudaMemcpyDeviceToHost), "copy y");
-    CK(cudaMemcpy(best_y, h->best_y, h->dd * 8, cudaMemcpyDeviceToHost), "copy y");
+    CK(h_get(h, res, h->res, sizeof(sc_ftp_result)), "copy result");
+    CK(h_get(h, &status, h->status, sizeof(int)), "copy status");
+    CK(h_get(h, y_tilde, h->y_tilde, h->dd * 8), "copy y");
+    CK(h_get(h, best_y, h->best_y, h->dd * 8), "copy y");
     float ms = 0.f;
     cudaEventElapsedTime(&ms, h->ev0, h->ev1);
     res->kernel_ms = ms;
@@ -814,6 +859,11 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     if (status == SC_EOOM) {
         h->err = "the suffix window outgrew the window ring (raise SCMWU_RING_GB)";
         return SC_EOOM;
+    }
+    if (status == SC_ENCCL) {
+        h->broken = true;
+        h->err = "a peer rank did not arrive at the in-kernel exchange (timeout)";
+        return SC_ENCCL;
     }
     if (status != SC_OK) { h->err = "kernel did not complete"; return SC_ECUDA; }
     return SC_OK;
@@ -851,11 +901,11 @@ static bool probe_throughput(sc_handle* h, std::vector<double>& thr) {
     const int st = ftp_impl(h, &a, &r, yt.data(), by.data(), dc);
     std::vector<long long> hc(2 * (size_t)G);
     const bool ok = st == SC_OK && r.passes >= 16 &&
-                    cudaMemcpy(hc.data(), dc, hc.size() * 8, cudaMemcpyDeviceToHost) ==
+                    h_get(h, hc.data(), dc, hc.size() * 8) ==
                         cudaSuccess;
     cudaFree(dc);
     // restore the call state the probe touched
-    cudaMemset(h->slots, 0, (size_t)kNumSlots * h->slot_len * 8);
+    h_zero(h, h->slots, (size_t)kNumSlots * h->slot_len * 8);
     h->has_sep = h->has_callmin = false;
     h->pass_total = 0;
     h->err.clear();
@@ -964,8 +1014,8 @@ int sc_set_globals(sc_handle* h, const double* red0, const double* v1, double g1
     if (!h || !red0) return SC_EARG;
     CK(cudaSetDevice(h->prob.device), "set device");
     for (int j = 0; j < h->rw; ++j) h->red0_h[j] = red0[j];
-    CK(cudaMemcpy(h->red0, red0, h->rw * 8, cudaMemcpyHostToDevice), "copy red0");
-    if (v1) CK(cudaMemcpy(h->v1, v1, h->prob.d * 8, cudaMemcpyHostToDevice), "copy anchor");
+    CK(h_put(h, h->red0, red0, h->rw * 8), "copy red0");
+    if (v1) CK(h_put(h, h->v1, v1, h->prob.d * 8), "copy anchor");
     h->g1 = g1;
     return SC_OK;
 }
@@ -979,7 +1029,8 @@ int sc_ipc_handle(sc_handle* h, void* out64) {
     CK(cudaSetDevice(h->prob.device), "set device");
     if (!h->mbox_base) {
         CK(cudaMalloc(&h->mbox_base, mbox_bytes(h)), "alloc mailbox");
-        CK(cudaMemset(h->mbox_base, 0, mbox_bytes(h)), "zero mailbox");
+        CK(h_zero(h, h->mbox_base, mbox_bytes(h)), "zero mailbox");
+        CK(cudaStreamSynchronize(h->stream), "zero mailbox");   // peers read it next
     }
     cudaIpcMemHandle_t ih;
     CK(cudaIpcGetMemHandle(&ih, h->mbox_base), "ipc handle");
@@ -1009,15 +1060,16 @@ int sc_iterate(sc_handle* h, double* out) {
     const int64_t first = h->prob.kind == SC_SES && h->prob.row0 == 0 ? 1 : 0;
     const int64_t size = h->prob.kind == SC_SES ? (n - first) * (h->prob.d + 1) : n;
     double* buf = nullptr;
-    CK(cudaMalloc(&buf, (size_t)std::max<int64_t>(size, 1) * 8), "alloc iterate");
+    CK(pool_alloc((void**)&buf, (size_t)std::max<int64_t>(size, 1) * 8, h->prob.device, h->stream),
+       "alloc iterate");
     // the `last` slot holds the latest iterate's state (written by the last sc_ftp)
     iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
         h->X, h->radii, n, h->prob.n1_local, h->prob.d, h->ld, h->prob.kind,
         h->slots + 4 * h->slot_len, h->dd, h->prob.rho, h->last_alpha, buf, first);
     h->launches += 1;
     cudaError_t e = cudaStreamSynchronize(h->stream);
-    if (e == cudaSuccess) e = cudaMemcpy(out, buf, (size_t)size * 8, cudaMemcpyDeviceToHost);
-    cudaFree(buf);
+    if (e == cudaSuccess) e = h_get(h, out, buf, (size_t)size * 8);
+    pool_free(buf, h->stream);
     if (e != cudaSuccess) return cuda_fail(h, e, "iterate");
     return SC_OK;
 }
@@ -1027,11 +1079,11 @@ int sc_pd_commit(sc_handle* h, int32_t which) {
     if (which != 0 && which != 1 && which != 2) return SC_EARG;
     CK(cudaSetDevice(h->prob.device), "set device");
     if (which == 2) {   // back to the t = 0 state (uniform pair)
-        CK(cudaMemset(h->slots + 3 * h->slot_len, 0, h->slot_len * 8), "reset pair");
+        CK(h_zero(h, h->slots + 3 * h->slot_len, h->slot_len * 8), "reset pair");
         return SC_OK;
     }
     const double* src = h->slots + (which == 0 ? 1 : 2) * h->slot_len;
-    CK(cudaMemcpy(h->slots + 3 * h->slot_len, src, h->slot_len * 8, cudaMemcpyDeviceToDevice),
+    CK(h_copy(h, h->slots + 3 * h->slot_len, src, h->slot_len * 8, cudaMemcpyDeviceToDevice),
        "commit");
     return SC_OK;
 }
@@ -1042,16 +1094,14 @@ int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
     const int64_t n = h->prob.n_local, n1 = h->prob.n1_local;
     const int d = h->prob.d;
     double* buf = nullptr;
-    CK(cudaMalloc(&buf, (size_t)n * 8), "alloc pair");
+    CK(pool_alloc((void**)&buf, (size_t)n * 8, h->prob.device, h->stream), "alloc pair");
     // e_i * T from the committed state (T cancels in the normalisation below)
     std::vector<double> slot(h->slot_len);
-    CK(cudaMemcpy(slot.data(), h->slots + 3 * h->slot_len, h->slot_len * 8,
-                  cudaMemcpyDeviceToHost), "copy slot");
+    CK(h_get(h, slot.data(), h->slots + 3 * h->slot_len, h->slot_len * 8), "copy slot");
     IterState* st = reinterpret_cast<IterState*>(slot.data() + h->dd + (h->dd & 1));
     if (st->T == 0.0) {   // never committed: uniform weights (t = 0 state)
         st->T = 1.0; st->eta = 1.0; st->t = 0.0; st->shift = 0.0;
-        CK(cudaMemcpy(h->slots + 3 * h->slot_len, slot.data(), h->slot_len * 8,
-                      cudaMemcpyHostToDevice), "init slot");
+        CK(h_put(h, h->slots + 3 * h->slot_len, slot.data(), h->slot_len * 8), "init slot");
     }
     iterate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(
         h->X, h->radii, n, n1, d, h->ld, SC_SVM, h->slots + 3 * h->slot_len, h->dd, h->prob.rho,
@@ -1059,8 +1109,8 @@ int sc_pd_pair(sc_handle* h, double* mu, double* gam, double* dist) {
     h->launches += 1;
     std::vector<double> e(n);
     cudaError_t ce = cudaStreamSynchronize(h->stream);
-    if (ce == cudaSuccess) ce = cudaMemcpy(e.data(), buf, (size_t)n * 8, cudaMemcpyDeviceToHost);
-    cudaFree(buf);
+    if (ce == cudaSuccess) ce = h_get(h, e.data(), buf, (size_t)n * 8);
+    pool_free(buf, h->stream);
     if (ce != cudaSuccess) return cuda_fail(h, ce, "pd pair");
     if (h->prob.world > 1) {   // sharded: raw local weights, the host normalises globally
         for (int64_t i = 0; i < n1; ++i) mu[i] = e[i];
@@ -1112,7 +1162,7 @@ int sc_debug_timing(sc_handle* h, double* out) {
     if (!h || !out) return SC_EARG;
     if (!h->timing) { for (int i = 0; i < 9 + 6 * 160 + 7; ++i) out[i] = 0.0; return SC_OK; }
     long long t[16 + 6 * 160 + 16];
-    CK(cudaMemcpy(t, h->timing, sizeof(t), cudaMemcpyDeviceToHost), "copy timing");
+    CK(h_get(h, t, h->timing, sizeof(t)), "copy timing");
     for (int i = 0; i < 9; ++i) out[i] = (double)t[i];
     for (int i = 0; i < 6 * 160; ++i) out[9 + i] = (double)t[16 + i];
     for (int i = 0; i < 7; ++i) out[9 + 6 * 160 + i] = (double)t[16 + 6 * 160 + i];
@@ -1136,6 +1186,7 @@ void sc_destroy(sc_handle* h) {
     if (h->mk0) cudaEventDestroy(h->mk0);
     if (h->mk1) cudaEventDestroy(h->mk1);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->pool_open) pool_handle_close(h->prob.device);
     delete h;
 }
 

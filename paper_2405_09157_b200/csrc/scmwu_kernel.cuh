@@ -183,6 +183,7 @@ struct KParams {
     int64_t pass_base;         // passes run by earlier calls (mailbox parity / flag epochs)
     double* mbox[kMaxWorld];   // rank r's mailbox data [2][world][rw] (peer pointers)
     unsigned long long* mflag[kMaxWorld];   // rank r's arrival flags [world]
+    long long xtimeout;        // cycles a rank waits for a peer's exchange flag
     uint32_t stage_stride;     // bytes per ring stage
     uint32_t rad_off;          // byte offset of the radii inside a stage
 };
@@ -255,11 +256,20 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // The CTA's writes are ordered before thread 0's release by bar.sync (release is
 // cumulative); the other threads' reads are ordered after its acquire by the second
 // bar.sync.  No full fences: one L2 reduction plus the acquire polling.
-__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target) {
+// `abort` (optional): a launch-wide abort word; a CTA that finds it set stops waiting, sets
+// sflag[1] and leaves the pass loop, so no CTA is left spinning in a barrier that the
+// aborting CTAs never reach (multi-GPU exchange failure).
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned long long target,
+                                             const unsigned long long* abort = nullptr,
+                                             volatile int* sflag = nullptr) {
     consumer_sync();
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
         while (ld_acquire(bar) < target) {
+            if (abort != nullptr && *(volatile const unsigned long long*)abort != 0) {
+                sflag[1] = 1;
+                break;
+            }
 #if defined(SCMWU_POLL_NS) && SCMWU_POLL_NS > 0
             __nanosleep(SCMWU_POLL_NS);   // A/B: back off instead of hammering the L2 line
 #endif
@@ -267,6 +277,9 @@ __device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned l
     }
     consumer_sync();
 }
+// word of the (zeroed per launch) barrier buffer that carries the abort decision; the
+// emulated-rank counters use words 8 .. 8 * (kMaxWorld + 1)
+constexpr int kAbortWord = 96;
 
 // --------------------------------------------------------------------------------------
 // combine operators of the reduced layout
@@ -847,7 +860,10 @@ enum FoldMode { kFoldTwoBarriers = 0, kFoldRedundant = 1, kFoldLast = 2 };
 // Multi-GPU exchange (after this rank's columns went out to every mailbox and the
 // local grid barrier): raise our flag on every rank, wait for every rank's flag, fold
 // the rank vectors in rank order into `red`.  Flags are monotone pass counters across
-// calls (no reset race); a 2^37-cycle timeout reports a missing peer via flags[1].
+// calls (no reset race).  A peer missing for p.xtimeout cycles sets the launch-wide abort
+// word: every CTA of this launch then leaves its barrier or poll and the pass loop, and the
+// call returns SC_ENCCL (the handle is marked unusable: the flag epochs of the ranks no
+// longer agree).
 // Out of line: it must not cost the streaming loop registers.
 // The rank a CTA belongs to.  Real multi-GPU (world > 1): every CTA of this GPU is rank
 // `shard`.  Emulated ranks on one GPU (vworld > 1, tests): the grid is split into vworld
@@ -897,13 +913,22 @@ static __device__ __noinline__ void rank_exchange(const KParams& p, const RankGr
     if (tid < g.W) {
         const long long t0 = clock64();
         unsigned long long v;
+        volatile unsigned long long* abort = p.bar + kAbortWord;
         do {
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
                          : "=l"(v) : "l"(p.mflag[g.rank] + tid) : "memory");
-            if (clock64() - t0 > (1ll << 37)) { flags[1] = 1; break; }
-        } while (v < want);
+            if (v >= want) break;
+            if (*abort != 0) { flags[1] = 1; break; }
+            if (clock64() - t0 > p.xtimeout) {
+                flags[1] = 1;
+                *abort = 1;
+                __threadfence();
+                break;
+            }
+        } while (true);
     }
     consumer_sync();
+    if (flags[1]) return;
     const double* mb = p.mbox[g.rank] + (size_t)((p.pass_base + pass_idx) & 1) * g.W * p.rw;
     for (int j = tid; j < p.rw; j += kNW * 32) {
         const int op = red_op(KIND, j);
@@ -1063,6 +1088,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
 
     int pass_idx = 0;
     unsigned long long nbar = 0;
+    // multi-GPU (real or emulated ranks): barriers also watch the launch-wide abort word
+    const unsigned long long* abort_w =
+        kMultiGpu && (p.world > 1 || p.vworld > 1) ? p.bar + kAbortWord : nullptr;
     // columns of the reduced vector folded by this CTA
     const RankGroup grp = rank_group(p, b);
     const int lb = b - grp.first;                 // index of this CTA within its rank
@@ -1195,10 +1223,14 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             consumer_sync();
             if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_arr));
 #endif
-            grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G);
+            grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G, abort_w, m.flags);
 #ifdef SCMWU_PHASE_TIMING
             if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_rel));
 #endif
+            if (m.flags[1]) {   // another CTA gave up on a peer: leave without folding
+                if (b == 0 && tid == 0) *p.status = SC_ENCCL;
+                break;
+            }
             SCMWU_TMARK(3)
             // column-distributed fold over this rank's G partials: warp per column, fixed
             // tree
@@ -1235,10 +1267,10 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
                 }
             }
             SCMWU_TMARK(4)
-            grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G);
+            grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G, abort_w, m.flags);
             SCMWU_TMARK(5)
             if (kMultiGpu && grp.W > 1) {
-                rank_exchange<KIND>(p, grp, m.red, m.flags, pass_idx);
+                if (!m.flags[1]) rank_exchange<KIND>(p, grp, m.red, m.flags, pass_idx);
             } else {
                 for (int j = tid; j < p.rw; j += kNW * 32) m.red[j] = __ldcg(p.redg + j);
             }

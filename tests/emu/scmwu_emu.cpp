@@ -148,6 +148,7 @@ static void pass_svm(const sc_handle* h, const PassParams& pp, const double* W,
 extern "C" {
 
 int sc_version(void) { return 1000; }
+int sc_pool_trim(int32_t) { return SC_OK; }   // no device pool on the host
 
 void emu_set_exchange(sc_handle* h, emu_exchange_fn fn) {
     if (h) h->exchange = fn;

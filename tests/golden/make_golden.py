@@ -8,6 +8,9 @@ it writes under tests/golden/ are committed and are what the tests read.
     python tests/golden/make_golden.py calls      # per-call solve_ftp/refine_run records
     python tests/golden/make_golden.py long       # C1 and n=2000 solves, threads 1/2/4/8
     python tests/golden/make_golden.py baselines  # meb_baseline / gilbert_baseline records
+    python tests/golden/make_golden.py headline KIND N THREADS
+        # one headline-regime solve (eps=1e-3, d=100: SES uniform-ball / SVM gap 1)
+        # with its per-call records -> tests/golden/headline/KIND_nN_tTHREADS.json
 
 Instances are NOT stored: tests regenerate them from (n, d, seed, dist) with
 paper_2405_09157_b200.instances, whose bit-exactness against the reference
@@ -376,6 +379,39 @@ def gen_baselines():
     dump("baselines.json", out)
 
 
+# ---------------------------------------------------------------- headline regime
+# BASELINE configs[1..4] run at eps=1e-3, d=100 (SES uniform-ball, SVM gap 1); these
+# record the reference's own solves of the same families at sizes it finishes in
+# minutes to hours, so the device's refine/stop behaviour can be compared with it.
+def gen_headline(kind: str, n: int, threads: int):
+    eps = 1e-3
+    t0 = time.time()
+    cfg = RunConfig(eps=eps, threads=threads)
+    if kind == "ses":
+        args = (n, 100, 0, "uniform-ball")
+        inst = instances.gen_ses(*args)
+        (r, s), calls = record_calls(lambda: ses.solve_ses(inst, eps, cfg))
+        rec = _solve_ses_rec(r, s)
+        D, _, _ = ses.ses_range(inst)
+    else:
+        args = (n // 2, n - n // 2, 100, 0, 1.0)
+        inst, _ = instances.gen_svm(*args)
+        (r, s), calls = record_calls(lambda: svm.solve_svm(inst, eps, cfg))
+        rec = _solve_svm_rec(r, s)
+        D = inst.max_norm
+    wall = time.time() - t0
+    for c in calls:  # the per-call y vectors are not needed here; keep the files small
+        c["result"].pop("y_tilde", None)
+        c["result"].pop("best_y", None)
+    out = {"kind": kind, "inst": list(args), "eps": eps, "threads": threads,
+           "wall_s": wall, "D": _f(D), "s_per_iter": wall / max(1, rec["iterations"]),
+           "solve": rec, "calls": calls}
+    os.makedirs(os.path.join(HERE, "headline"), exist_ok=True)
+    dump(os.path.join("headline", f"{kind}_n{n}_t{threads}.json"), out)
+    print(kind, args, threads, rec["iterations"], rec["termination"], f"{wall:.1f}s",
+          file=sys.stderr)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "quick"
     if what == "quick":
@@ -388,5 +424,7 @@ if __name__ == "__main__":
         gen_calls()
     elif what == "long":
         gen_long()
+    elif what == "headline":
+        gen_headline(sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))
     else:
         raise SystemExit(f"unknown group {what}")

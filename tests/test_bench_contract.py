@@ -1,5 +1,5 @@
-"""bench.py's JSON-line contract on the CPU-only arm (the reference arm times the oracle
-port; the GPU arm is exercised by the driver on a B200)."""
+"""bench.py's JSON-line contract on the CPU-only arm (the reference arm times the
+reference in baseline/_ref, else the oracle port; the GPU arm runs on a B200)."""
 import json
 import os
 import subprocess
@@ -22,5 +22,7 @@ def test_reference_arm_json_line():
               "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is False
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    # the time-to-eps uses the reference's own recorded iteration count (long.json, C1)
+    assert d["config"]["reference_iterations"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]

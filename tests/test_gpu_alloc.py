@@ -1,7 +1,8 @@
 """Handle memory on the e2e path: X, radii and the window ring come from the
-stream-ordered pool and are reused by the next handle; buffers above the retained size
-(SCMWU_POOL_GB, default 4 GiB) use cudaMalloc.  Creating and destroying handles must not
-leak device memory, and a handle on reused memory computes exactly what a fresh one does.
+engine's private stream-ordered pool and are reused by the next handle (up to
+SCMWU_POOL_GB, default 12 GiB, stays mapped; sc_pool_trim releases it); larger buffers use
+cudaMalloc.  Creating and destroying handles must not leak device memory, and a handle on
+reused memory computes exactly what a fresh one does.
 """
 import numpy as np
 import pytest
@@ -39,9 +40,15 @@ def test_handles_reuse_pool_memory_without_leaking():
     assert _free() >= free0 - SLACK
 
 
-def test_large_buffer_bypasses_pool():
+def test_pool_retains_then_trims():
+    from paper_2405_09157_b200 import _native as nat
+    eng = nat.cuda_engine()
+    eng.trim_pool(0)
     free0 = _free()
-    for _ in range(2):   # 7e6 x 100 fp64 = 5.6 GB > the 4 GiB retained by the pool
+    for _ in range(2):   # 7e6 x 100 fp64 = 5.6 GB: pooled, reused by the second handle
         dev = gen_ses_device(7_000_000, 100, 1, "uniform-ball")
         dev.close()
-        assert _free() >= free0 - SLACK
+        kept = free0 - _free()
+        assert kept <= (12 << 30) + SLACK      # at most the retained size stays mapped
+    eng.trim_pool(0)
+    assert _free() >= free0 - SLACK          # and sc_pool_trim returns it
