@@ -20,6 +20,11 @@
  *                   (PrimalCertificate.p / DualFeasible.p_last, R/meta.py:123,132).
  *   sc_pd_commit /  keep the best polytope-distance pair across calls and materialise
  *   sc_pd_pair      it (best_pd in R/svm.py:171-181, read at :229-231).
+ *   sc_solve        replaces meta.adaptive_search (R/meta.py:656-781) with _Bracket
+ *                   (R/meta.py:576-653) as driven by solve_ses / solve_svm (R/ses.py:
+ *                   171-187, R/svm.py:189-214): the seed certificate, every bracketing
+ *                   test and refine round, and the final enclosure check run inside ONE
+ *                   persistent kernel launch (no host round trip between the tests).
  *
  * Conventions: plain pointers and sizes, caller-owned host buffers are only read
  * (or written) during the call, all device memory is owned by the handle, one
@@ -122,6 +127,53 @@ typedef struct {
                                  others were certified by the bound of DESIGN.md §4.4) */
 } sc_ftp_result;
 
+/* Whole-solve residency (sc_solve): the arguments of adaptive_search as solve_ses /
+ * solve_svm call it (R/ses.py:178-183, R/svm.py:207-214). */
+typedef struct {
+    double eps;                /* search eps (SVM: 0.4 * eps, R/svm.py:150, :209) */
+    double L0, U0;             /* initial range */
+    double delta;              /* EarlyStopConfig */
+    int32_t patience;
+    int32_t enabled;
+    int64_t cap;               /* iteration_cap_override, or < 0 for none */
+    int64_t ceil_ln_r;         /* math.ceil(ln r) */
+    int64_t refine_horizon;    /* REFINE_HORIZON (R/meta.py:452) */
+    double zero_lower_floor;   /* SVM: _INFEASIBLE_FLOOR * 2D; NaN = none */
+    int32_t on_primal;         /* SVM: separations certify the pd distance (R/svm.py:201-204) */
+    int32_t max_steps;         /* capacity of the caller's step log (<= 400 steps happen) */
+} sc_solve_args;
+
+/* One SearchStep (R/meta.py:150-160). */
+typedef struct {
+    double alpha, eps;
+    int64_t iteration_bound, iterations;
+    int32_t separated, reason; /* enum sc_reason */
+} sc_search_step;
+
+enum sc_termination { SC_TERM_ITERATION_CAP = 0, SC_TERM_RANGE_CONVERGED = 1,
+                      SC_TERM_EARLY_STOPPED = 2 };
+
+typedef struct {
+    double lower, upper;       /* the bracket at exit (SearchResult.lower / upper) */
+    double best_value;         /* SearchResult.best_value */
+    int32_t has_best;          /* a certified payload exists (else RuntimeError) */
+    int32_t termination;       /* enum sc_termination */
+    int64_t total_iterations;
+    int32_t search_steps;
+    int32_t has_pd;            /* SVM: a pd_counter distance was committed (best_pd) */
+    double pd_dist;            /* SVM: best_pd["dist"] */
+    double seed_f;             /* progress of the seed point (R/ses.py:175, R/svm.py:198) */
+    double final_f;            /* SES: progress at the returned centre (slack = final_f -
+                                  best_value, R/ses.py:187) */
+    /* width violation (status SC_EWIDTH): the failing test's level and iteration */
+    double width_alpha;
+    int64_t width_iteration;
+    double width_norm;
+    int64_t passes;
+    float kernel_ms;
+    int64_t width_passes;
+} sc_solve_result;
+
 /* X: row-major host rows.  SES: n rows (centres), radii n values.  SVM: the n1
  * rows of P; X_tail (if not NULL) holds the n - n1 rows of Q, otherwise X
  * holds all n rows; radii must be NULL. */
@@ -165,6 +217,11 @@ int sc_gilbert_baseline(sc_handle* h, double gap_tol, int64_t max_iters, double*
 int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
            double* y_tilde /* dual_dim */, double* best_y /* dual_dim */);
 int sc_progress(sc_handle* h, const double* y /* d values */, double* f);
+/* A whole solve in one launch.  seed_y: the seed point's first d coordinates (SES the
+ * anchor centre v1, SVM the cluster-mean direction w0); best_y (dual_dim) receives
+ * SearchResult.best_y and steps the search log (args->max_steps entries). */
+int sc_solve(sc_handle* h, const sc_solve_args* args, const double* seed_y,
+             sc_solve_result* res, double* best_y, sc_search_step* steps);
 int sc_iterate(sc_handle* h, double* p /* SES (n-1)(d+1), SVM n */);
 int sc_pd_commit(sc_handle* h, int32_t which /* 0: call minimum, 1: separating iterate,
                                                 2: reset to the uniform pair */);

@@ -15,8 +15,9 @@ import os
 import numpy as np
 
 SC_SES, SC_SVM = 0, 1
+SC_PRIMAL, SC_DUAL = 0, 1
 SC_OK, SC_EARG, SC_ECUDA, SC_ENCCL, SC_EWIDTH, SC_EOOM = range(6)
-_REASONS = {0: "exhausted", 1: "early_stop", 2: "affirmative", 3: "refined"}
+_REASONS = {0: "separated", 1: "exhausted", 2: "early_stop", 3: "affirmative", 4: "refined"}
 _dp, _vp = ctypes.POINTER(ctypes.c_double), ctypes.c_void_p
 
 
@@ -140,7 +141,7 @@ class Device:
         best_f = res.best_f if res.has_best_f else None
         best_y = by.copy() if res.has_best_f else None
         best_c = res.best_counter if res.has_best_counter else None
-        if res.kind == 1:   # SC_PRIMAL
+        if res.kind == SC_PRIMAL:
             self.last_sep_dist = res.sep_dist
             return meta.PrimalCertificate(p=None, alpha=alpha, iterations=res.iterations,
                                           oracle_value=res.oracle_value, best_progress=best_f,

@@ -77,12 +77,42 @@ class ScFtpResult(ctypes.Structure):
                 ("width_passes", ctypes.c_int64)]
 
 
+class ScSolveArgs(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("L0", ctypes.c_double), ("U0", ctypes.c_double),
+                ("delta", ctypes.c_double), ("patience", ctypes.c_int32),
+                ("enabled", ctypes.c_int32), ("cap", ctypes.c_int64),
+                ("ceil_ln_r", ctypes.c_int64), ("refine_horizon", ctypes.c_int64),
+                ("zero_lower_floor", ctypes.c_double), ("on_primal", ctypes.c_int32),
+                ("max_steps", ctypes.c_int32)]
+
+
+class ScSearchStep(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_double), ("eps", ctypes.c_double),
+                ("iteration_bound", ctypes.c_int64), ("iterations", ctypes.c_int64),
+                ("separated", ctypes.c_int32), ("reason", ctypes.c_int32)]
+
+
+class ScSolveResult(ctypes.Structure):
+    _fields_ = [("lower", ctypes.c_double), ("upper", ctypes.c_double),
+                ("best_value", ctypes.c_double), ("has_best", ctypes.c_int32),
+                ("termination", ctypes.c_int32), ("total_iterations", ctypes.c_int64),
+                ("search_steps", ctypes.c_int32), ("has_pd", ctypes.c_int32),
+                ("pd_dist", ctypes.c_double), ("seed_f", ctypes.c_double),
+                ("final_f", ctypes.c_double), ("width_alpha", ctypes.c_double),
+                ("width_iteration", ctypes.c_int64), ("width_norm", ctypes.c_double),
+                ("passes", ctypes.c_int64), ("kernel_ms", ctypes.c_float),
+                ("width_passes", ctypes.c_int64)]
+
+
+SC_TERMINATIONS = {0: "IterationCap", 1: "RangeConverged", 2: "EarlyStopped"}
+MAX_SEARCH_STEPS = 400
+
 EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "sc_pd_pair",
            "sc_set_grid", "sc_info", "sc_mark", "sc_elapsed", "sc_launches", "sc_debug_timing",
            "sc_local_red0", "sc_progress_parts", "sc_set_globals", "sc_ipc_handle",
            "sc_connect", "sc_last_error", "sc_destroy", "sc_version", "sc_create_generated",
            "sc_set_range", "sc_read_rows", "sc_meb_baseline", "sc_gilbert_baseline",
-           "sc_pool_trim")
+           "sc_pool_trim", "sc_solve")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -119,6 +149,9 @@ class Engine:
         lib.sc_destroy.restype = None
         lib.sc_version.restype = ctypes.c_int
         lib.sc_pool_trim.argtypes = [ctypes.c_int32]
+        lib.sc_solve.argtypes = [vp, ctypes.POINTER(ScSolveArgs), _dp,
+                                 ctypes.POINTER(ScSolveResult), _dp,
+                                 ctypes.POINTER(ScSearchStep)]
         lib.sc_mark.argtypes = [vp, ctypes.c_int32]
         lib.sc_elapsed.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
         lib.sc_launches.argtypes = [vp]
@@ -256,6 +289,20 @@ class Handle:
         o.kernel_ms = float(res.kernel_ms)
         o.width_passes = int(res.width_passes)
         return o
+
+    def solve(self, args: ScSolveArgs, seed_y):
+        """A whole adaptive search in one launch (sc_solve).  Returns (status, result,
+        best_y, steps)."""
+        seed = np.ascontiguousarray(np.asarray(seed_y, dtype=np.float64)[: self.d])
+        res = ScSolveResult()
+        by = np.zeros(self.dual_dim)
+        steps = (ScSearchStep * max(1, args.max_steps))()
+        st = self.engine.lib.sc_solve(self.h, ctypes.byref(args), _ptr(seed), ctypes.byref(res),
+                                      _ptr(by), steps)
+        self.calls += 1
+        if st not in (SC_OK, SC_EWIDTH):
+            self._check(st, "sc_solve")
+        return st, res, by, [steps[i] for i in range(min(res.search_steps, args.max_steps))]
 
     def progress(self, y) -> float:
         y = np.ascontiguousarray(np.asarray(y, dtype=np.float64)[: self.d])

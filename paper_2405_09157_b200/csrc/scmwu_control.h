@@ -152,6 +152,7 @@ struct CtlSlots {
     double* pd_callmin;  // SVM: state at the call's smallest counter distance
     double* pd_sep;      // SVM: state of the separating iterate
     double* last;        // state of the latest iterate (for sc_iterate)
+    double* pd_best;     // SVM: the committed best_pd state (sc_pd_pair reads it)
 };
 
 template <class L>
@@ -736,6 +737,276 @@ SC_UNROLL4
         }
         (void)tt;
         return kContinue;
+    }
+};
+
+
+// ======================================================================================
+// Whole-solve residency (sc_solve): meta.adaptive_search (R/meta.py:656-781) with _Bracket
+// (R/meta.py:576-653), as solve_ses / solve_svm drive it (R/ses.py:171-187,
+// R/svm.py:189-214), run between the streaming passes of ONE persistent launch.  Every
+// feasibility test is the Control above; the search decides the next test's level and
+// arguments from the previous result exactly as the reference does (same constants, same
+// operation order), so all CTAs (and all ranks) take identical decisions.
+//
+// Two extra "progress passes" stream X for ses_progress / svm_progress at a given point
+// (the seed certificate and, SES, the final enclosure check): a check pass of the kernel
+// with the point in the window-average slot, every learner weight 1 (eta = 0).
+constexpr int kMaxSearchSteps = 400;     // R/meta.py:449
+constexpr int64_t kBracketTestCap = 2048; // R/meta.py:450
+constexpr int64_t kRefineStart = 2048;    // R/meta.py:451
+constexpr int kMaxRefineRounds = 12;      // R/meta.py:453
+constexpr int64_t kBudgetClamp = (int64_t)1 << 62;
+
+enum SearchPhase { kSeedPass = 0, kBracket = 1, kRefine = 2, kSlackPass = 3, kFinished = 4 };
+
+template <class L>
+struct Search {
+    sc_solve_args sa;
+    double R, rho, ln_r;
+    bool is_max;
+    int kind, d, dd;
+    // _Bracket
+    double Lb, Ub, gain_floor;
+    bool has_best; double best_f;          // best_y lives in `sbest` (shared memory)
+    // adaptive_search state
+    int phase, nsteps, rounds;
+    int64_t total, test_cap, h;
+    bool capped, floored;
+    double alpha, eps_i;
+    int64_t Ti, full, horizon;
+    // svm.py best_pd (R/svm.py:171-181): committed on the device
+    bool has_pd; double pd_best;
+    double seed_f, final_f;
+    int status;
+    double w_alpha; int64_t w_iter; double w_norm;
+    double* sbest;                         // smem vector (dd): the bracket's best_y
+    double* yprog;                         // smem vector: the progress pass's point
+    sc_search_step* log;                   // device log (written by the writer)
+    bool writer;
+
+    SC_HD static int64_t bound(double R_, double rho_, double lnr, double e, double a) {
+        // iteration_bound (R/meta.py:208-213): ceil(4 R^2 rho^2 ln r / (eps^2 alpha^2)), the
+        // same left-to-right operation order (x**2 == x*x exactly), clamped like the callers
+        const double v = ceil(4.0 * (R_ * R_) * (rho_ * rho_) * lnr / ((e * e) * (a * a)));
+        return v >= (double)kBudgetClamp ? kBudgetClamp : (int64_t)v;
+    }
+    SC_HD void tighten_dual(double f) {
+        if (is_max) Ub = Ub < f ? Ub : f; else Lb = Lb > f ? Lb : f;
+    }
+    SC_HD void tighten_primal(double f) {
+        if (is_max) Lb = Lb > f ? Lb : f; else Ub = Ub < f ? Ub : f;
+    }
+    SC_HD bool converged(double e) const {
+        const double span = Ub - Lb;
+        const double ref = Lb > 0.0 ? Lb : (is_max ? span / 3.0 : 2.0 * span / 3.0);
+        return span < e * ref;
+    }
+
+    // ---- progress pass at y (first d coordinates of `src`)
+    template <class C>
+    SC_HD int progress_pass(C& ctl, const double* src, PassParams* pp) {
+        for (int j = L::lane(); j < dd; j += L::nl()) yprog[j] = j < d ? src[j] : 0.0;
+        L::sync();
+        (void)ctl;
+        if (L::lane() == 0) {
+            pp->t = 1.0; pp->alpha = 0.0; pp->eta_rho = 0.0; pp->shift = 0.0;
+            pp->S1 = pp->S2 = pp->s1p = pp->s2p = 0.0;
+            pp->check = 1; pp->width = 0; pp->action = kPass;
+        }
+        return kPass;
+    }
+    // the progress value the pass produced (ses_progress / svm_progress)
+    template <class C>
+    SC_HD double progress_value(C& ctl, const double* red) {
+        if (kind == SC_SES) return red[kS_Fw];
+        double acc = 0.0;
+        for (int j = L::lane(); j < d; j += L::nl()) acc += yprog[j] * yprog[j];
+        (void)ctl;
+        return C::svm_margin(red[kV_minPy], red[kV_maxQy], sqrt(L::sum(acc)));
+    }
+
+    // ---- start: bracket seeded by the progress of the seed point (R/ses.py:174-176,
+    // R/svm.py:194-199, R/meta.py:700-701)
+    template <class C>
+    SC_HD int begin(C& ctl, const sc_solve_args& args, const double* seed, PassParams* pp) {
+        sa = args;
+        is_max = kind == SC_SES;
+        Lb = sa.L0; Ub = sa.U0;
+        gain_floor = sa.delta > sa.eps / 10.0 ? sa.delta : sa.eps / 10.0;
+        has_best = false; best_f = 0.0;
+        nsteps = 0; rounds = 0; total = 0; capped = false; floored = false;
+        test_cap = sa.cap >= 0 && sa.cap < kBracketTestCap ? sa.cap : kBracketTestCap;
+        h = kRefineStart;
+        has_pd = false; pd_best = 0.0;
+        seed_f = 0.0; final_f = 0.0; status = SC_OK;
+        w_alpha = 0.0; w_iter = 0; w_norm = 0.0;
+        phase = kSeedPass;
+        return progress_pass(ctl, seed, pp);
+    }
+
+    // ---- after every streaming pass
+    template <class C>
+    SC_HD int after_pass(C& ctl, const double* red, const double* red0, double* y_tilde,
+                         PassParams* pp) {
+        if (phase == kSeedPass) {
+            const double f = progress_value(ctl, red);
+            seed_f = f;
+            has_best = true; best_f = f;                       // _Bracket.seed
+            for (int j = L::lane(); j < dd; j += L::nl())
+                sbest[j] = j < d ? yprog[j] : (kind == SC_SES ? f : 0.0);
+            tighten_dual(f);
+            phase = kBracket;
+            return next_test(ctl, red0, y_tilde, pp);
+        }
+        if (phase == kSlackPass) {
+            final_f = progress_value(ctl, red);
+            phase = kFinished;
+            return kDone;
+        }
+        int act = ctl.after_pass(red, red0, y_tilde, pp);
+        if (act == kPass) return kPass;
+        return test_done(ctl, red0, y_tilde, pp);
+    }
+
+    // a feasibility test ended (ctl.res holds its outcome): absorb it.  Returns kCont to
+    // choose the next test, kFin to end the search, kErr after a failed test.
+    enum { kCont = 0, kFin = 1, kErr = 2 };
+    template <class C>
+    SC_HD int absorb(C& ctl) {
+        const sc_ftp_result& r = *ctl.res;
+        if (ctl.status != SC_OK) {            // WidthViolationError / ring overflow: stop
+            status = ctl.status;
+            w_alpha = alpha; w_iter = r.width_iteration; w_norm = r.width_norm;
+            phase = kFinished;
+            return kErr;
+        }
+        // DeviceProblem.run: the call's smallest pd_counter distance becomes best_pd
+        if (kind == SC_SVM && r.has_counter_min && (!has_pd || r.counter_min < pd_best)) {
+            ctl.copy_slot(ctl.s.pd_best, ctl.s.pd_callmin);
+            has_pd = true; pd_best = r.counter_min;
+        }
+        total += r.iterations;
+        const bool primal = r.kind == SC_PRIMAL;
+        if (phase == kBracket && sa.cap >= 0 && sa.cap < Ti && !primal &&
+            r.reason == SC_REASON_EXHAUSTED && r.iterations >= sa.cap)
+            capped = true;
+        // _Bracket.absorb (R/meta.py:603-644)
+        const double span_before = Ub - Lb;
+        bool improved = false;
+        if (primal) {
+            tighten_primal(alpha);                     // separation is exact
+            if (sa.on_primal) {                        // pd_counter(cert.p) (R/svm.py:201-204)
+                const double c = r.sep_dist;
+                if (!has_pd || c < pd_best) {
+                    ctl.copy_slot(ctl.s.pd_best, ctl.s.pd_sep);
+                    has_pd = true; pd_best = c;
+                }
+                tighten_primal(c);
+            }
+        } else {
+            tighten_dual(r.value);                     // regret-certified claim
+        }
+        if (r.has_best_f) {
+            const double f = r.best_f;
+            const bool better = !has_best || (is_max ? f < best_f : f > best_f);
+            if (better) {
+                if (has_best && fabs(best_f - f) > gain_floor * fabs(best_f)) improved = true;
+                has_best = true; best_f = f;
+                for (int j = L::lane(); j < dd; j += L::nl()) sbest[j] = ctl.v.besty[j];
+            }
+            tighten_dual(best_f);
+        }
+        if (r.has_best_counter) tighten_primal(r.best_counter);
+        const bool productive = improved || (Ub - Lb) < span_before * (1.0 - 2e-2);
+        if (writer && L::lane() == 0 && nsteps < sa.max_steps) {   // SearchStep
+            sc_search_step& st = log[nsteps];
+            st.alpha = alpha; st.eps = phase == kBracket ? eps_i : sa.eps;
+            st.iteration_bound = Ti; st.iterations = r.iterations;
+            st.separated = primal ? 1 : 0; st.reason = primal ? SC_REASON_SEPARATED : r.reason;
+        }
+        ++nsteps;
+        L::sync();
+        if (phase == kBracket) {
+            if (!productive) phase = kRefine;          // the bracketing loop breaks
+            return kCont;
+        }
+        ++rounds;
+        if (!productive && horizon >= full) return kFin;
+        h = h * 4 < sa.refine_horizon ? h * 4 : sa.refine_horizon;
+        return kCont;
+    }
+
+    template <class C>
+    SC_HD int test_done(C& ctl, const double* red0, double* y_tilde, PassParams* pp) {
+        const int r = absorb(ctl);
+        if (r == kErr) return kDone;
+        if (r == kFin) return finish(ctl, pp);
+        return next_test(ctl, red0, y_tilde, pp);
+    }
+
+    // choose and start the next test; a test can end before its first pass (iterate 1 is
+    // precomputed), so loop until one needs a pass or the search ends
+    template <class C>
+    SC_HD int next_test(C& ctl, const double* red0, double* y_tilde, PassParams* pp) {
+        for (;;) {
+            sc_ftp_args a;
+            a.has_progress = 1; a.delta = sa.delta; a.patience = sa.patience;
+            a.enabled = sa.enabled; a.ceil_ln_r = sa.ceil_ln_r;
+            if (phase == kBracket) {                     // R/meta.py:705-730
+                bool stop = nsteps >= kMaxSearchSteps || converged(sa.eps);
+                const double span = Ub - Lb;
+                if (!stop && !isnan(sa.zero_lower_floor) && Lb == 0.0 &&
+                    span < sa.zero_lower_floor) {
+                    floored = true;
+                    stop = true;
+                }
+                if (stop) { phase = kRefine; continue; }
+                alpha = is_max ? Lb + span / 3.0 : Lb + 2.0 * span / 3.0;
+                eps_i = span / (3.0 * alpha);
+                Ti = bound(R, rho, ln_r, eps_i, alpha);
+                a.mode = SC_MODE_FTP; a.alpha = alpha; a.eps = eps_i;
+                a.budget = Ti < test_cap ? Ti : test_cap;
+                a.horizon = 0; a.gain_rel = NAN; a.lo = -INFINITY; a.hi = INFINITY;
+                a.target = NAN;
+            } else if (phase == kRefine) {               // R/meta.py:732-763
+                if (floored || rounds >= kMaxRefineRounds || converged(sa.eps) ||
+                    nsteps >= kMaxSearchSteps)
+                    return finish(ctl, pp);
+                alpha = (Lb + Ub) / 2.0;
+                if (alpha <= 0.0) return finish(ctl, pp);
+                Ti = bound(R, rho, ln_r, sa.eps, alpha);
+                full = Ti < sa.refine_horizon ? Ti : sa.refine_horizon;
+                if (sa.cap >= 0 && sa.cap < full) full = sa.cap;
+                horizon = h < full ? h : full;
+                a.mode = SC_MODE_REFINE; a.alpha = alpha; a.eps = NAN; a.budget = 0;
+                a.horizon = horizon > sa.ceil_ln_r ? horizon : sa.ceil_ln_r;   // R/meta.py:479
+                a.gain_rel = sa.delta > sa.eps / 20.0 ? sa.delta : sa.eps / 20.0;
+                a.lo = Lb; a.hi = Ub; a.target = sa.eps;
+            } else {
+                return kDone;
+            }
+            if (ctl.begin(a, red0, y_tilde, nullptr, pp) == kPass) return kPass;
+            const int r = absorb(ctl);
+            if (r == kErr) return kDone;
+            if (r == kFin) return finish(ctl, pp);
+        }
+    }
+
+    template <class C>
+    SC_HD int finish(C& ctl, PassParams* pp) {
+        if (kind == SC_SES && has_best) {                // final enclosure check (R/ses.py:187)
+            phase = kSlackPass;
+            return progress_pass(ctl, sbest, pp);
+        }
+        phase = kFinished;
+        return kDone;
+    }
+
+    SC_HD int termination() const {
+        if (capped) return SC_TERM_ITERATION_CAP;
+        if (converged(sa.eps)) return SC_TERM_RANGE_CONVERGED;
+        return SC_TERM_EARLY_STOPPED;
     }
 };
 

@@ -33,6 +33,9 @@ struct sc_handle {
     int* status = nullptr;
     long long* timing = nullptr;     // SCMWU_TIMING=1: per-phase cycle sums of the last call
     double* v1 = nullptr;            // SES anchor row
+    sc_search_step* steps_dev = nullptr;   // sc_solve: the search log
+    int steps_cap = 0;
+    sc_solve_result* sres_dev = nullptr;
     // sharding: this rank's mailbox (flags + 2 x world x rw doubles) and the peers'
     void* mbox_base = nullptr;
     void* peer_base[kMaxWorld] = {};

@@ -277,9 +277,15 @@ static void pool_handle_close(int device) {
     if (dp.handles > 0) dp.handles -= 1;
 }
 
+// Off by default: the equal cyclic partition by CTA index makes the fixed-order fold, and
+// with it every result, bitwise reproducible across processes and boxes (the calibrated
+// weights are re-measured per process).  Measured on B200 (profiles/r02_kernel_ab.md): at
+// configs[3] (SES n = 10^7, d = 100) the calibrated partition does not help (per-CTA pass
+// times spread 1.82M-2.00M cycles with it, 1.91M-1.99M without; 1252-1311 vs 1250-1290
+// us/pass); at n = 10^6 it saved 2-3 % (round 1).  SCMWU_BALANCE=1 opts in.
 static bool balance_enabled() {
     const char* e = getenv("SCMWU_BALANCE");
-    return e == nullptr || atoi(e) != 0;
+    return e != nullptr && atoi(e) != 0;
 }
 
 static const std::vector<double>* sm_weights(sc_handle* h) {
@@ -736,27 +742,12 @@ int sc_set_grid(sc_handle* h, int32_t grid) {
     return configure(h, grid);
 }
 
-static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
-                    double* y_tilde, double* best_y, long long* slot_cycles) {
-    if (!h || !args || !res || !y_tilde || !best_y) return SC_EARG;
-    memset(res, 0, sizeof(*res));
-    if (h->broken) {
-        h->err = "handle unusable after a multi-GPU exchange failure";
-        return SC_ENCCL;
-    }
-    if (args->mode != SC_MODE_FTP && args->mode != SC_MODE_REFINE) return SC_EARG;
-    if (!(args->alpha > 0.0)) { h->err = "alpha must be positive"; return SC_EARG; }
-    const int64_t T = args->mode == SC_MODE_FTP ? args->budget : args->horizon;
-    if (T < 0 || (args->mode == SC_MODE_REFINE && T < 1)) {
-        h->err = "budget/horizon out of range";
-        return SC_EARG;
-    }
-    CK(cudaSetDevice(h->prob.device), "set device");
-    // window history: max(64, T/2) + 2 entries (the largest rung is <= T)
+// window history for runs of up to T iterations: max(64, T/2) + 2 entries, capped at
+// SCMWU_RING_GB (default 2 GiB: 2.6M entries at d = 100, 0.5M at d = 512); a run whose
+// window outgrows the ring stops with SC_EOOM instead of overwriting live entries
+static int ensure_ring(sc_handle* h, int64_t T) {
     int64_t need = std::max<int64_t>(kLadderBase, T / 2) + 2;
     const int dd8 = (h->dd + 1) & ~1;                             // 16-byte ring entries
-    // capped at SCMWU_RING_GB (default 2 GiB: 2.6M entries at d = 100, 0.5M at d = 512); a run
-    // whose window outgrows the ring stops with SC_EOOM instead of overwriting live entries
     double ring_gb = 2.0;
     if (const char* e = getenv("SCMWU_RING_GB")) ring_gb = std::max(1e-6, atof(e));
     const int64_t cap_lim = std::max<int64_t>(kLadderBase + 2, (int64_t)(ring_gb * 1073741824.0) / (dd8 * 8));
@@ -768,12 +759,15 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
            "alloc window ring");
         h->ring_cap = need;
     }
-    KParams p;
+    return SC_OK;
+}
+
+// kernel parameters common to sc_ftp and sc_solve
+static int fill_params(sc_handle* h, KParams& p, long long* slot_cycles) {
     memset(&p, 0, sizeof(p));
     p.kind = h->prob.kind; p.d = h->prob.d; p.ld = h->ld; p.dd = h->dd; p.rw = h->rw; p.pw = h->pw;
     p.G = h->grid; p.gP = h->gP; p.tile_rows = h->tile_rows; p.stages = h->stages;
     p.resident = h->resident; p.n = h->prob.n; p.n1 = h->prob.n1;
-    // every CTA re-reads all partials when that is cheap (<= 192 KB per CTA)
     // grid reduction scheme (SCMWU_FOLD=0 two barriers, 1 redundant, 2 last arriver)
     // measured on B200 (profiles/r01_overhead.md): two barriers 8.3 us/pass at C1,
     // last-arriver 16.9 us (147 CTAs poll one line while one CTA folds), redundant worse
@@ -799,8 +793,7 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     p.D = h->prob.D; p.g1 = h->g1;
     p.red0 = h->red0; p.partials = h->partials; p.redg = h->redg; p.bar = h->bar;
     p.ring = h->ring; p.ring_cap = h->ring_cap; p.slots = h->slots; p.slot_len = h->slot_len;
-    h->last_alpha = args->alpha;
-    p.args = *args; p.res = h->res; p.y_tilde = h->y_tilde; p.best_y = h->best_y;
+    p.res = h->res; p.y_tilde = h->y_tilde; p.best_y = h->best_y;
     p.status = h->status; p.stage_stride = h->stage_stride; p.rad_off = h->rad_off;
     if (!h->timing && getenv("SCMWU_TIMING")) {
         CK(cudaMalloc(&h->timing, (16 + 6 * 160 + 16) * 8), "alloc timing");
@@ -833,6 +826,11 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
             p.mbox[r] = reinterpret_cast<double*>(static_cast<char*>(h->peer_base[r]) + 64 * 8);
         }
     }
+    return SC_OK;
+}
+
+// one cooperative launch of the persistent kernel; returns the kernel's status word
+static int launch(sc_handle* h, KParams& p, int* status, float* ms) {
     CK(cudaMemsetAsync(h->bar, 0, 1024, h->stream), "reset barrier");
     CK(cudaMemsetAsync(h->res, 0, sizeof(sc_ftp_result), h->stream), "reset result");
     CK(cudaMemsetAsync(h->status, 0xff, sizeof(int), h->stream), "reset status");
@@ -844,17 +842,14 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     h->launches += 1;
     CK(cudaEventRecord(h->ev1, h->stream), "event");
     CK(cudaStreamSynchronize(h->stream), "persistent kernel");
-    int status = -1;
-    CK(h_get(h, res, h->res, sizeof(sc_ftp_result)), "copy result");
-    CK(h_get(h, &status, h->status, sizeof(int)), "copy status");
-    CK(h_get(h, y_tilde, h->y_tilde, h->dd * 8), "copy y");
-    CK(h_get(h, best_y, h->best_y, h->dd * 8), "copy y");
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, h->ev0, h->ev1);
-    res->kernel_ms = ms;
-    h->pass_total += res->passes;
-    h->has_callmin = res->has_counter_min != 0;
-    h->has_sep = res->kind == SC_PRIMAL;
+    *status = -1;
+    CK(h_get(h, status, h->status, sizeof(int)), "copy status");
+    *ms = 0.f;
+    cudaEventElapsedTime(ms, h->ev0, h->ev1);
+    return SC_OK;
+}
+
+static int kernel_status(sc_handle* h, int status) {
     if (status == SC_EWIDTH) { h->err = "width violation"; return SC_EWIDTH; }
     if (status == SC_EOOM) {
         h->err = "the suffix window outgrew the window ring (raise SCMWU_RING_GB)";
@@ -867,6 +862,43 @@ static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
     }
     if (status != SC_OK) { h->err = "kernel did not complete"; return SC_ECUDA; }
     return SC_OK;
+}
+
+static int ftp_impl(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res,
+                    double* y_tilde, double* best_y, long long* slot_cycles) {
+    if (!h || !args || !res || !y_tilde || !best_y) return SC_EARG;
+    memset(res, 0, sizeof(*res));
+    if (h->broken) {
+        h->err = "handle unusable after a multi-GPU exchange failure";
+        return SC_ENCCL;
+    }
+    if (args->mode != SC_MODE_FTP && args->mode != SC_MODE_REFINE) return SC_EARG;
+    if (!(args->alpha > 0.0)) { h->err = "alpha must be positive"; return SC_EARG; }
+    const int64_t T = args->mode == SC_MODE_FTP ? args->budget : args->horizon;
+    if (T < 0 || (args->mode == SC_MODE_REFINE && T < 1)) {
+        h->err = "budget/horizon out of range";
+        return SC_EARG;
+    }
+    CK(cudaSetDevice(h->prob.device), "set device");
+    int st = ensure_ring(h, T);
+    if (st != SC_OK) return st;
+    KParams p;
+    st = fill_params(h, p, slot_cycles);
+    if (st != SC_OK) return st;
+    h->last_alpha = args->alpha;
+    p.args = *args;
+    int status = -1;
+    float ms = 0.f;
+    st = launch(h, p, &status, &ms);
+    if (st != SC_OK) return st;
+    CK(h_get(h, res, h->res, sizeof(sc_ftp_result)), "copy result");
+    CK(h_get(h, y_tilde, h->y_tilde, h->dd * 8), "copy y");
+    CK(h_get(h, best_y, h->best_y, h->dd * 8), "copy y");
+    res->kernel_ms = ms;
+    h->pass_total += res->passes;
+    h->has_callmin = res->has_counter_min != 0;
+    h->has_sep = res->kind == SC_PRIMAL;
+    return kernel_status(h, status);
 }
 
 // Balanced-partition calibration (see sm_weights): refine runs at the feasible end of the
@@ -954,6 +986,71 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
         }
     }
     return ftp_impl(h, args, res, y_tilde, best_y, nullptr);
+}
+
+int sc_solve(sc_handle* h, const sc_solve_args* args, const double* seed_y,
+             sc_solve_result* res, double* best_y, sc_search_step* steps) {
+    if (!h || !args || !seed_y || !res || !best_y || (!steps && args->max_steps > 0))
+        return SC_EARG;
+    memset(res, 0, sizeof(*res));
+    if (h->broken) {
+        h->err = "handle unusable after a multi-GPU exchange failure";
+        return SC_ENCCL;
+    }
+    if (!(args->eps > 0.0 && args->eps < 1.0) || !(args->L0 >= 0.0 && args->L0 < args->U0) ||
+        args->max_steps < 0 || args->refine_horizon < 1) {
+        h->err = "bad search arguments";
+        return SC_EARG;
+    }
+    CK(cudaSetDevice(h->prob.device), "set device");
+    if (h->balance_ok && !h->by_smid && !h->calib_tried) {   // opt-in (SCMWU_BALANCE=1)
+        if (sm_weights(h) != nullptr) {
+            h->calib_tried = true;
+            configure(h, h->grid_req);
+        } else {
+            calibrate_partition(h);
+        }
+    }
+    // the longest feasibility test of a search: a bracketing test (<= 2048) or a refine
+    // round (<= refine_horizon)
+    int st = ensure_ring(h, std::max<int64_t>(args->refine_horizon, kBracketTestCap));
+    if (st != SC_OK) return st;
+    const int nsteps = std::max(1, args->max_steps);
+    if (h->steps_cap < nsteps) {
+        pool_free(h->steps_dev, h->stream);
+        h->steps_dev = nullptr;
+        CK(pool_alloc((void**)&h->steps_dev, (size_t)nsteps * sizeof(sc_search_step),
+                      h->prob.device, h->stream), "alloc step log");
+        h->steps_cap = nsteps;
+    }
+    if (!h->sres_dev)
+        CK(pool_alloc((void**)&h->sres_dev, sizeof(sc_solve_result), h->prob.device, h->stream),
+           "alloc solve result");
+    KParams p;
+    st = fill_params(h, p, nullptr);
+    if (st != SC_OK) return st;
+    CK(h_put(h, h->yvec, seed_y, (size_t)h->prob.d * 8), "copy seed");
+    CK(h_zero(h, h->slots + 3 * h->slot_len, h->slot_len * 8), "reset best_pd");  // per solve
+    CK(h_zero(h, h->sres_dev, sizeof(sc_solve_result)), "reset solve result");
+    p.solve = 1;
+    p.sargs = *args;
+    p.seed = h->yvec;
+    p.sres = h->sres_dev;
+    p.steps = h->steps_dev;
+    p.args.mode = SC_MODE_FTP;   // unused: every test's arguments come from the search
+    int status = -1;
+    float ms = 0.f;
+    st = launch(h, p, &status, &ms);
+    if (st != SC_OK) return st;
+    CK(h_get(h, res, h->sres_dev, sizeof(sc_solve_result)), "copy solve result");
+    CK(h_get(h, best_y, h->best_y, h->dd * 8), "copy y");
+    const int ns = std::min(res->search_steps, args->max_steps);
+    if (ns > 0) CK(h_get(h, steps, h->steps_dev, (size_t)ns * sizeof(sc_search_step)), "copy steps");
+    res->kernel_ms = ms;
+    h->pass_total += res->passes;
+    h->has_callmin = false;
+    h->has_sep = false;
+    return kernel_status(h, status);
 }
 
 int sc_progress_parts(sc_handle* h, const double* y, double* out) {
@@ -1176,7 +1273,7 @@ void sc_destroy(sc_handle* h) {
     cudaSetDevice(h->prob.device);
     void* bufs[] = {h->X, h->radii, h->red0, h->partials, h->redg, h->row_begin, h->bar, h->timing,
                     h->ring, h->slots, h->res, h->y_tilde, h->best_y, h->scratch, h->yvec,
-                    h->status, h->v1, h->mbox_base};
+                    h->status, h->v1, h->mbox_base, h->steps_dev, h->sres_dev};
     for (int r = 0; r < kMaxWorld && h->vworld <= 1; ++r)   // emulated ranks: own memory
         if (h->peer_base[r] && h->peer_base[r] != h->mbox_base) cudaIpcCloseMemHandle(h->peer_base[r]);
     for (void* b : bufs)   // pool or cudaMalloc memory (pool_free tells them apart)

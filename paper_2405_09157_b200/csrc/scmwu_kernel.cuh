@@ -184,6 +184,12 @@ struct KParams {
     double* mbox[kMaxWorld];   // rank r's mailbox data [2][world][rw] (peer pointers)
     unsigned long long* mflag[kMaxWorld];   // rank r's arrival flags [world]
     long long xtimeout;        // cycles a rank waits for a peer's exchange flag
+    // whole-solve residency (sc_solve): the adaptive search runs between the passes
+    int solve;
+    sc_solve_args sargs;
+    const double* seed;        // the seed point (d values)
+    sc_solve_result* sres;
+    sc_search_step* steps;
     uint32_t stage_stride;     // bytes per ring stage
     uint32_t rad_off;          // byte offset of the radii inside a stage
 };
@@ -376,6 +382,8 @@ struct SmemMap {
     sc_ftp_result* resd;
     void* ctl;         // the control state between tails (warp 0 holds it in registers
                        // only while the tail runs, so the passes get those registers)
+    void* srch;        // the adaptive-search state (sc_solve)
+    double* sbest;     // the search's best_y (dd8)
     volatile int* flags;  // spare
     unsigned char* ring;
 };
@@ -391,6 +399,7 @@ __host__ __device__ inline size_t smem_fixed_bytes(int dd, int rw, int pw, int n
     b += (size_t)kNW * ((pw + 1) & ~1) * 8;            // warp partials
     b += sizeof(PassParams) + sizeof(sc_ftp_result) + 16 * 4 + 64;
     b += sizeof(Control<WarpLanes>) + 16;
+    b += sizeof(Search<WarpLanes>) + 16 + (size_t)dd8_of(dd) * 8;   // sc_solve state
     return (b + 127) & ~(size_t)127;
 }
 
@@ -422,6 +431,12 @@ __device__ inline SmemMap carve(unsigned char* base, const KParams& p) {
     off = (off + 15) & ~(size_t)15;
     m.ctl = base + off;
     off += sizeof(Control<WarpLanes>);
+    off = (off + 15) & ~(size_t)15;
+    m.srch = base + off;
+    off += sizeof(Search<WarpLanes>);
+    off = (off + 15) & ~(size_t)15;
+    m.sbest = reinterpret_cast<double*>(base + off);
+    off += (size_t)dd8 * 8;
     m.flags = reinterpret_cast<volatile int*>(base + off);
     return m;
 }
@@ -638,6 +653,8 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
         const double* xs = reinterpret_cast<const double*>(st);
         const double* rs = reinterpret_cast<const double*>(st + p.rad_off) + (a & 1);
+        const int r = myk * RPW + grp;              // the row this lane finishes (phase B)
+        const double g = r < nr ? rs[r] : 0.0;
         // phase A: per-lane partial sums of NB rows; the differences stay in registers
         // for phase C (one shared-memory read and one DFMA less per element)
         double v[NV][NB];
@@ -672,10 +689,8 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         }
         reduce_scatter<LPR, NB, NV>(v, l);
         // phase B: per-row scalar math, one row per lane (DUP copies)
-        const int r = myk * RPW + grp;
         double cc = 0.0;
         if (r < nr) {
-            const double g = rs[r];
             const double ra = sqrt(v[0][0]);
             if (primary) {
                 F = fmax(F, fma(ra, inv_t, g));
@@ -704,6 +719,8 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
 #pragma unroll
             for (int c = 0; c < CPL; ++c) Sd[c] = fma(ck, dfk[k][c], Sd[c]);
         }
+        // (releasing the stage right after phase A instead: SES C2 134 -> 137 us/pass, C4
+        // unchanged, profiles/r02_kernel_ab.md; SVM keeps the early release)
         release_stage(p, m, r0, r1, warp, ws);
     }
     // warp reduction (all 32 lanes; non-primary lanes hold identities)
@@ -793,6 +810,9 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
             v[0][k] = dW; v[1][k] = dw;
             if (CHECK) { v[2][k] = dy; v[3][k] = dz; }
         }
+        // the tile is in registers: hand the stage back before the row math, so its refill
+        // is in flight during phases B and C (C3 shape 126.0 -> 125.5 us/pass)
+        release_stage(p, m, r0, r1, warp, ws);
         reduce_scatter<LPR, NB, NV>(v, l);
         const int r = myk * RPW + grp;
         double e = 0.0;
@@ -821,7 +841,6 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
 #pragma unroll
             for (int c = 0; c < CPL; ++c) G[c] = fma(ek, xk[k][c], G[c]);
         }
-        release_stage(p, m, r0, r1, warp, ws);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1002,6 +1021,38 @@ static __device__ __noinline__ void fold_all(const KParams& p, const double* par
 }
 
 // --------------------------------------------------------------------------------------
+// control tails (warp 0 of every CTA, between passes).  Out of line: the control state is
+// loaded from and stored back to shared memory here, so none of it is live in the
+// streaming loop's register allocation.
+template <int KIND>
+static __device__ __noinline__ int ctl_tail(const KParams& p, const SmemMap& m,
+                                            double* y_tilde, PassParams* pp) {
+    Control<WarpLanes>* const sm = reinterpret_cast<Control<WarpLanes>*>(m.ctl);
+    Control<WarpLanes> ctl = *sm;
+    const int act = ctl.after_pass(m.red, p.red0, y_tilde, pp);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) *sm = ctl;
+    __syncwarp();
+    return act;
+}
+template <int KIND>
+static __device__ __noinline__ int solve_tail(const KParams& p, const SmemMap& m,
+                                              double* y_tilde, PassParams* pp) {
+    Control<WarpLanes>* const csm = reinterpret_cast<Control<WarpLanes>*>(m.ctl);
+    Search<WarpLanes>* const ssm = reinterpret_cast<Search<WarpLanes>*>(m.srch);
+    Control<WarpLanes> ctl = *csm;
+    Search<WarpLanes> srch = *ssm;
+    const int act = srch.after_pass(ctl, m.red, p.red0, y_tilde, pp);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+        *csm = ctl;
+        *ssm = srch;
+    }
+    __syncwarp();
+    return act;
+}
+
+// --------------------------------------------------------------------------------------
 // the persistent kernel
 template <int KIND, int LPR, int CPL, int NB, bool FULL>
 __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constant__ KParams p) {
@@ -1047,15 +1098,16 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     // registers for the tail and stores it back, so it is dead (no registers) during the
     // streaming passes.  Every lane holds identical scalars; lane 0 stores them.
     using Ctl = Control<WarpLanes>;
+    using Srch = Search<WarpLanes>;
     Ctl* const ctl_sm = reinterpret_cast<Ctl*>(m.ctl);
     PassParams* pp = m.pp;
-    double* y_tilde = b == 0 ? p.y_tilde : m.ytd;
+    double* y_tilde = b == 0 && !p.solve ? p.y_tilde : m.ytd;
     if (warp == 0) {
         Ctl ctl;
         ctl.kind = KIND; ctl.d = p.d; ctl.dd = p.dd; ctl.is_max = KIND == SC_SES;
         ctl.rho = p.rho; ctl.inv_rho = p.inv_rho; ctl.R = p.R; ctl.ln_r = p.ln_r;
         ctl.D = p.D; ctl.g1 = p.g1;
-        ctl.res = b == 0 ? p.res : m.resd;
+        ctl.res = b == 0 && !p.solve ? p.res : m.resd;
         ctl.writer = b == 0;
         double* V = m.vec;
         ctl.v = CtlVecs{V, V + dd8, V + 2 * dd8, V + 3 * dd8, V + 4 * dd8, V + 5 * dd8,
@@ -1072,13 +1124,24 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
         }
 #endif
         ctl.s = CtlSlots{p.ring, p.ring_cap, dd8, p.slots, p.slots + sl, p.slots + 2 * sl,
-                         p.slots + 4 * sl};
+                         p.slots + 4 * sl, p.slots + 3 * sl};
         for (int j = lane; j < dd8; j += 32) {
             for (int q = 0; q < 10; ++q) V[q * dd8 + j] = 0.0;
             if (KIND == SC_SES && j < p.d) V[9 * dd8 + j] = p.v1[j];   // anchor v1
         }
         __syncwarp();
-        int act = ctl.begin(p.args, p.red0, y_tilde, nullptr, pp);
+        int act;
+        if (p.solve) {
+            Srch srch;
+            srch.R = p.R; srch.rho = p.rho; srch.ln_r = p.ln_r;
+            srch.kind = KIND; srch.d = p.d; srch.dd = p.dd;
+            srch.sbest = m.sbest; srch.yprog = ctl.v.ywin; srch.log = p.steps;
+            srch.writer = b == 0;
+            act = srch.begin(ctl, p.sargs, p.seed, pp);
+            if (lane == 0) *reinterpret_cast<Srch*>(m.srch) = srch;
+        } else {
+            act = ctl.begin(p.args, p.red0, y_tilde, nullptr, pp);
+        }
         if (lane == 0) {
             pp->action = act;
             *ctl_sm = ctl;
@@ -1286,13 +1349,9 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             break;
         }
         if (warp == 0) {
-            Ctl ctl = *ctl_sm;
-            int act = ctl.after_pass(m.red, p.red0, y_tilde, pp);
-            __syncwarp();
-            if (lane == 0) {
-                pp->action = act;
-                *ctl_sm = ctl;
-            }
+            const int act = p.solve ? solve_tail<KIND>(p, m, y_tilde, pp)
+                                    : ctl_tail<KIND>(p, m, y_tilde, pp);
+            if (lane == 0) pp->action = act;
             stream_flush(p, m, r0, r1, warp, ws);
         }
         SCMWU_TMARK(7)
@@ -1326,7 +1385,24 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
     }
     // wait for the prefetched copies of the (never run) next pass, then publish (CTA 0)
     stream_drain(p, m, warp, ws);
-    if (b == 0 && warp == 0) {
+    if (b == 0 && warp == 0 && p.solve) {
+        __syncwarp();
+        const Srch* sr = reinterpret_cast<const Srch*>(m.srch);
+        for (int j = lane; j < p.dd; j += 32) p.best_y[j] = m.sbest[j];
+        if (lane == 0) {
+            sc_solve_result& o = *p.sres;
+            o.lower = sr->Lb; o.upper = sr->Ub; o.best_value = sr->best_f;
+            o.has_best = sr->has_best; o.termination = sr->termination();
+            o.total_iterations = sr->total; o.search_steps = sr->nsteps;
+            o.has_pd = sr->has_pd; o.pd_dist = sr->pd_best;
+            o.seed_f = sr->seed_f; o.final_f = sr->final_f;
+            o.width_alpha = sr->w_alpha; o.width_iteration = sr->w_iter;
+            o.width_norm = sr->w_norm;
+            o.passes = pass_idx;
+            o.width_passes = width_passes;
+            if (!m.flags[1]) *p.status = sr->status;
+        }
+    } else if (b == 0 && warp == 0) {
         __syncwarp();
         for (int j = lane; j < p.dd; j += 32) p.best_y[j] = ctl_sm->v.besty[j];
         if (lane == 0) {

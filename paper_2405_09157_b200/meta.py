@@ -16,6 +16,7 @@ inside a single persistent CUDA kernel.  ``adaptive_search`` stays on the host
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 from enum import Enum
 from typing import Callable, Optional, Union
@@ -400,6 +401,61 @@ class _Bracket:
         else:
             ref = span / 3.0 if self.is_max else 2.0 * span / 3.0
         return span < eps * ref
+
+
+def host_search_requested() -> bool:
+    """SCMWU_HOST_SEARCH=1: drive the adaptive search from the host, one launch per test
+    (the round-1 path; kept for A/B and for the parity tests of the device search)."""
+    return os.environ.get("SCMWU_HOST_SEARCH", "0") not in ("", "0")
+
+
+def resident_search(oracle: OracleSpec, L0: float, U0: float, eps: float,
+                    stopping: EarlyStopConfig | None, cap: int | None,
+                    seed_y: np.ndarray, on_primal: bool = False,
+                    zero_lower_floor: float | None = None,
+                    refine_horizon: int = REFINE_HORIZON):
+    """adaptive_search (R/meta.py:656-781) with the bracket, every test and the seed /
+    final progress passes inside ONE persistent kernel launch (sc_solve).  The seed
+    certificate is (progress(seed_y), (seed_y; f)) for SES and (progress(w0), (w0; 0; 0))
+    for SVM, exactly as solve_ses / solve_svm build it.  Returns (SearchResult, seed_f,
+    final_f): final_f is the progress at the returned centre (SES, R/ses.py:187)."""
+    if not 0.0 <= L0 < U0:
+        raise ValueError(f"need 0 <= L0 < U0, got [{L0}, {U0}]")
+    if not 0.0 < eps < 1.0:
+        raise ValueError("eps must be in (0, 1)")
+    if stopping is None:
+        stopping = EarlyStopConfig()
+    dev = oracle.device
+    ln_r = math.log(oracle.cone.rank)
+    args = nat.ScSolveArgs(eps=eps, L0=float(L0), U0=float(U0), delta=stopping.delta,
+                           patience=stopping.patience, enabled=int(bool(stopping.enabled)),
+                           cap=-1 if cap is None else int(cap), ceil_ln_r=math.ceil(ln_r),
+                           refine_horizon=refine_horizon,
+                           zero_lower_floor=(math.nan if zero_lower_floor is None
+                                             else zero_lower_floor),
+                           on_primal=int(bool(on_primal)), max_steps=nat.MAX_SEARCH_STEPS)
+    st, r, best_y, steps = dev.handle.solve(args, seed_y)
+    dev.calls += 1
+    dev.last_kernel_ms = float(r.kernel_ms)
+    dev.total_kernel_ms += float(r.kernel_ms)
+    dev.total_passes += int(r.passes)
+    dev.total_width_passes += int(r.width_passes)
+    if st == nat.SC_EWIDTH:
+        raise WidthViolationError(r.width_alpha, oracle.width_rho, int(r.width_iteration),
+                                  r.width_norm)
+    if r.has_pd:
+        dev.best_pd_dist = float(r.pd_dist)
+    if not r.has_best:
+        raise RuntimeError("search finished without any certified solution; "
+                           "pass an initial_certificate")
+    log = [SearchStep(s.alpha, s.eps, int(s.iteration_bound), int(s.iterations),
+                      bool(s.separated), nat.REASONS.get(s.reason, "?")) for s in steps]
+    res = SearchResult(lower=r.lower, upper=r.upper, best_value=r.best_value, best_y=best_y,
+                       last_primal=None, last_dual=None,
+                       total_iterations=int(r.total_iterations),
+                       search_steps=int(r.search_steps),
+                       termination=Termination(nat.SC_TERMINATIONS[r.termination]), steps=log)
+    return res, float(r.seed_f), float(r.final_f)
 
 
 def adaptive_search(oracle_factory: Callable[[float], OracleSpec], L0: float, U0: float,

@@ -250,7 +250,7 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     c.v = CtlVecs{ysum.data(), yprev.data(), wsum.data(), besty.data(), claimy.data(),
                   ywin.data(), zv.data(), ynew.data(), pU.data(), v1.data()};
     c.s = CtlSlots{h->ring.data(), cap, dd, h->pd_pending.data(), h->pd_callmin.data(),
-                   h->pd_sep.data(), h->last.data()};
+                   h->pd_sep.data(), h->last.data(), h->pd_best.data()};
     PassParams pp{};
     const int rw = red_width(h->prob.kind, d);
     std::vector<double> red(rw), loc(rw);
@@ -272,6 +272,67 @@ int sc_ftp(sc_handle* h, const sc_ftp_args* args, sc_ftp_result* res, double* y_
     res->width_passes = width_passes;
     if (c.status == SC_EWIDTH) return fail(h, SC_EWIDTH, "width violation");
     return c.status;
+}
+
+// sc_solve: the whole adaptive search between passes, the same Search state machine the
+// kernel runs (scmwu_control.h), driven by the host loop
+int sc_solve(sc_handle* h, const sc_solve_args* args, const double* seed_y,
+             sc_solve_result* res, double* best_y, sc_search_step* steps) {
+    if (!h || !args || !seed_y || !res || !best_y || (!steps && args->max_steps > 0))
+        return SC_EARG;
+    memset(res, 0, sizeof(*res));
+    const int d = h->prob.d, dd = h->dd;
+    if (h->prob.world > 1 && !h->exchange) return fail(h, SC_EARG, "no exchange callback");
+    const int64_t T = std::max<int64_t>(args->refine_horizon, kBracketTestCap);
+    int64_t cap = (T / 2 > kLadderBase ? T / 2 : kLadderBase) + 2;
+    if (cap > (1 << 21)) cap = (1 << 21);
+    h->ring.assign((size_t)cap * dd, 0.0);
+    h->pd_best.assign(h->pd_best.size(), 0.0);   // best_pd is per solve (R/svm.py:171)
+    std::vector<double> ysum(dd), yprev(dd), wsum(dd), besty(dd), claimy(dd), ywin(dd),
+        zv(dd), ynew(dd), pU(dd), v1(h->v1), sbest(dd), ytd(dd);
+    sc_ftp_result fres{};
+    Control<HostLanes> c;
+    c.kind = h->prob.kind; c.d = d; c.dd = dd;
+    c.is_max = h->prob.kind == SC_SES;
+    c.rho = h->prob.rho; c.inv_rho = 1.0 / h->prob.rho; c.R = h->prob.R;
+    c.ln_r = h->prob.ln_r; c.D = h->prob.D;
+    c.g1 = h->g1;
+    c.res = &fres; c.writer = true;
+    c.v = CtlVecs{ysum.data(), yprev.data(), wsum.data(), besty.data(), claimy.data(),
+                  ywin.data(), zv.data(), ynew.data(), pU.data(), v1.data()};
+    c.s = CtlSlots{h->ring.data(), cap, dd, h->pd_pending.data(), h->pd_callmin.data(),
+                   h->pd_sep.data(), h->last.data(), h->pd_best.data()};
+    Search<HostLanes> S;
+    S.R = h->prob.R; S.rho = h->prob.rho; S.ln_r = h->prob.ln_r;
+    S.kind = h->prob.kind; S.d = d; S.dd = dd;
+    S.sbest = sbest.data(); S.yprog = ywin.data(); S.log = steps; S.writer = true;
+    PassParams pp{};
+    const int rw = red_width(h->prob.kind, d);
+    std::vector<double> red(rw), loc(rw);
+    int act = S.begin(c, *args, seed_y, &pp);
+    int64_t passes = 0, width_passes = 0;
+    while (act == kPass) {
+        double* dst = h->prob.world > 1 ? loc.data() : red.data();
+        if (h->prob.kind == SC_SES && (pp.check || pp.width)) ++width_passes;
+        if (h->prob.kind == SC_SES)
+            pass_ses(h, pp, ysum.data(), yprev.data(), ywin.data(), dst);
+        else
+            pass_svm(h, pp, ysum.data(), yprev.data(), ywin.data(), zv.data(), dst);
+        if (h->prob.world > 1) h->exchange(loc.data(), rw, red.data());
+        ++passes;
+        act = S.after_pass(c, red.data(), h->red0.data(), ytd.data(), &pp);
+    }
+    for (int j = 0; j < dd; ++j) best_y[j] = sbest[j];
+    res->lower = S.Lb; res->upper = S.Ub; res->best_value = S.best_f;
+    res->has_best = S.has_best; res->termination = S.termination();
+    res->total_iterations = S.total; res->search_steps = S.nsteps;
+    res->has_pd = S.has_pd; res->pd_dist = S.pd_best;
+    res->seed_f = S.seed_f; res->final_f = S.final_f;
+    res->width_alpha = S.w_alpha; res->width_iteration = S.w_iter; res->width_norm = S.w_norm;
+    res->passes = passes; res->width_passes = width_passes;
+    if (S.status == SC_EWIDTH) return fail(h, SC_EWIDTH, "width violation");
+    if (S.status != SC_OK) return fail(h, S.status, "solve failed");
+    return SC_OK;
 }
 
 int sc_progress_parts(sc_handle* h, const double* y, double* out) {

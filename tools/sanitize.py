@@ -50,7 +50,8 @@ def case_gen():
 
 
 def case_balanced():
-    # >= 64 warp tiles per SM: the calibrated per-SM contiguous partition
+    # >= 64 warp tiles per SM: the calibrated per-SM contiguous partition (opt-in)
+    os.environ["SCMWU_BALANCE"] = "1"
     inst = devgen.gen_ses_device(400000, 100, 4, "uniform-ball")
     try:
         rep, sol = ses.solve_ses(inst, 3e-2)
@@ -63,6 +64,7 @@ def case_balanced():
         assert math.isfinite(sol.margin), sol
     finally:
         inst.close()
+    os.environ.pop("SCMWU_BALANCE")
 
 
 def case_baselines():
