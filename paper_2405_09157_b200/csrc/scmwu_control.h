@@ -93,7 +93,8 @@ SC_HD double sc_exp(double x) {
 }
 
 // ---- layout of one reduced pass vector ------------------------------------
-// SES: T, Lin, Rad, M (max lambda+), F (max progress of U/t), Wd (max residual
+// SES: T, K (= sum_i c_i |U - t v_i|^2, from which the tail forms the oracle's linear term,
+//      DESIGN.md §3), Rad, M (max lambda+), F (max progress of U/t), Wd (max residual
 //      eigen-magnitude of iteration t), Fw (max progress of the window avg),
 //      then Sd[d] = sum_i c_i (U - t v_i).
 // SVM: TP, TQ, M (max logit), minresP, minresQ, Wd (max |res|), minPW, maxQW,
@@ -401,23 +402,26 @@ SC_UNROLL4
                 return finish_sep(-INFINITY, k, red, y_tilde);
             }
             const double coef = -(eta * inv_rho) / Tt;
-            // one reduction for |s|^2 and s.v1: s.u = s.v1 + (alpha - g1) |s|^2 / |s|
-            double s2 = 0.0, sv = 0.0;
+            // one reduction for |s|^2, s.v1 and U.Sd: s.u = s.v1 + (alpha - g1) |s|^2 / |s|
+            double s2 = 0.0, sv = 0.0, us = 0.0;
 SC_UNROLL4
             for (int j = ln; j < d; j += nl) {
                 const double sj = coef * red[kS_Vec + j];
                 v.ynew[j] = sj;          // temporarily s
                 s2 = fma(sj, sj, s2);
                 sv = fma(sj, v.v1[j], sv);
+                us = fma(v.ysum[j], red[kS_Vec + j], us);
             }
-            L::sum2(s2, sv);
+            L::sum3(s2, sv, us);
             const double sn = sqrt(s2);
             const double am = a.alpha - g1;
             const double inv_sn = sn > 0.0 ? 1.0 / sn : 0.0;
 SC_UNROLL4
             for (int j = ln; j < d; j += nl) v.ynew[j] = fma(am * inv_sn, v.ynew[j], v.v1[j]);
             const double su = sn > 0.0 ? fma(am * inv_sn, s2, sv) : sv;
-            const double lin = coef * red[kS_Lin];
+            // sum_i c_i v_i.(U - t v_i) = (U . Sd - K) / t (v_i = (U - df_i) / t): the
+            // pass then needs no per-element dot product with v_i (0 at t = 0: U = 0)
+            const double lin = t > 0 ? coef * ((us - red[kS_Lin]) / (double)t) : 0.0;
             const double rad = red[kS_Rad] / (kSqrt2 * Tt);
             value = su + a.alpha / kSqrt2 - lin - rad;            // R/ses.py:123
             if (value < 0.0) return finish_sep(value, k, red, y_tilde);

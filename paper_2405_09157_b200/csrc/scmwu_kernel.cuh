@@ -98,6 +98,20 @@ struct WarpLanes {
 #endif
         return x;
     }
+    // three independent butterfly sums interleaved (ILP)
+    __host__ __device__ static void sum3(double& a, double& b, double& c) {
+#ifdef __CUDA_ARCH__
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double x = __shfl_xor_sync(0xffffffffu, a, o);
+            const double y = __shfl_xor_sync(0xffffffffu, b, o);
+            const double z = __shfl_xor_sync(0xffffffffu, c, o);
+            a += x;
+            b += y;
+            c += z;
+        }
+#endif
+    }
     // two independent butterfly sums interleaved (ILP)
     __host__ __device__ static void sum2(double& a, double& b) {
 #ifdef __CUDA_ARCH__
@@ -621,7 +635,8 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
     constexpr bool WIDTH = MODE >= 1;
     constexpr int RPW = 32 / LPR;
     constexpr int DUP = LPR / NB;
-    constexpr int NV = 2 + (WIDTH ? 1 : 0) + (CHECK ? 1 : 0);
+    // per-row sums: |df|^2, then |y_prev - v|^2 (WIDTH), |y_win - v|^2 (CHECK)
+    constexpr int NV = 1 + (WIDTH ? 1 : 0) + (CHECK ? 1 : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
     const int d = p.d, ld = p.ld, dd8 = dd8_of(p.dd);
@@ -645,7 +660,8 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
     const double inv_t = 1.0 / t;
     const int myk = l / DUP;                 // row-group whose sums this lane ends up with
     const bool primary = (l % DUP) == 0;
-    double T = 0, Lin = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
+    // K = sum_i c_i |df_i|^2 (the tail forms Lin = (U . Sd - K) / t from it)
+    double T = 0, K = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
     for (int q = 0; q < ws.cnt; ++q) {
         const int j = warp + q * kNW;
         const unsigned char* st = acquire_stage(p, m, warp, ws, pass_idx);
@@ -663,7 +679,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         for (int k = 0; k < NB; ++k) {
             const int r = (k ^ myk) * RPW + grp;   // slot k: row-group k ^ myk
             const double* xr = xs + (size_t)(r < nr ? r : 0) * ld + l;
-            double sa = 0, sl = 0, sw = 0, sf = 0;
+            double sa = 0, sw = 0, sf = 0;
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
                 dfk[k][c] = 0.0;
@@ -672,7 +688,6 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                     const double df = fma(-t, x, U[c]);
                     dfk[k][c] = df;
                     sa = fma(df, df, sa);
-                    sl = fma(x, df, sl);
                     if (WIDTH) {
                         const double wv = up[WIDTH ? c : 0] - x;
                         sw = fma(wv, wv, sw);
@@ -683,8 +698,8 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                     }
                 }
             }
-            v[0][k] = sa; v[1][k] = sl;
-            if (WIDTH) v[WIDTH ? 2 : 0][k] = sw;
+            v[0][k] = sa;
+            if (WIDTH) v[WIDTH ? 1 : 0][k] = sw;
             if (CHECK) v[NV - 1][k] = sf;
         }
         reduce_scatter<LPR, NB, NV>(v, l);
@@ -704,10 +719,10 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
                 cc = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
                 if (primary) {
                     T += A + B;
-                    Lin = fma(cc, v[1][0], Lin);
+                    K = fma(cc, v[0][0], K);
                     Rad = fma(g, A + B, Rad);
                     M = fmax(M, lp);
-                    if (WIDTH) Wd = fmax(Wd, (fabs(al - g) + sqrt(v[WIDTH ? 2 : 0][0])) * kInvSqrt2);
+                    if (WIDTH) Wd = fmax(Wd, (fabs(al - g) + sqrt(v[WIDTH ? 1 : 0][0])) * kInvSqrt2);
                 }
             }
         }
@@ -727,7 +742,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         T += __shfl_xor_sync(0xffffffffu, T, o);
-        Lin += __shfl_xor_sync(0xffffffffu, Lin, o);
+        K += __shfl_xor_sync(0xffffffffu, K, o);
         Rad += __shfl_xor_sync(0xffffffffu, Rad, o);
         M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
         F = fmax(F, __shfl_xor_sync(0xffffffffu, F, o));
@@ -742,7 +757,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         if (grp == 0 && j < d) wp[kS_Vec + j] = s;
     }
     if (lane == 0) {
-        wp[kS_T] = T; wp[kS_Lin] = Lin; wp[kS_Rad] = Rad; wp[kS_M] = M;
+        wp[kS_T] = T; wp[kS_Lin] = K; wp[kS_Rad] = Rad; wp[kS_M] = M;
         wp[kS_F] = F; wp[kS_Wd] = Wd; wp[kS_Fw] = Fw;
     }
 }

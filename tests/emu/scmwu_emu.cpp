@@ -31,6 +31,7 @@ struct HostLanes {
     static int nl() { return 1; }
     static double sum(double x) { return x; }
     static void sum2(double&, double&) {}
+    static void sum3(double&, double&, double&) {}
     static void sync() {}
     static double ldcg(const double* p) { return *p; }
     static void prefetch(double* dst, const double* src, int n) {
@@ -69,18 +70,17 @@ static void pass_ses(const sc_handle* h, const PassParams& pp, const double* U,
                      const double* up, const double* yw, double* red) {
     const int d = h->prob.d;
     const int64_t n = h->prob.n_local;
-    double T = 0, Lin = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
+    double T = 0, K = 0, Rad = 0, M = -INFINITY, F = -INFINITY, Wd = 0, Fw = -INFINITY;
     std::vector<double> Sd(d, 0.0), df(d);
     const double t = pp.t, er = pp.eta_rho, al = pp.alpha;
     for (int64_t i = 0; i < n; ++i) {
         const double* v = &h->X[i * d];
         const double g = h->radii[i];
-        double a = 0, l = 0, w2 = 0, f2 = 0;
+        double a = 0, w2 = 0, f2 = 0;
         for (int j = 0; j < d; ++j) {
             double x = fma(-t, v[j], U[j]);
             df[j] = x;
             a = fma(x, x, a);
-            l = fma(v[j], x, l);
             double w = up[j] - v[j];
             w2 = fma(w, w, w2);
             if (pp.check) { double y = yw[j] - v[j]; f2 = fma(y, y, f2); }
@@ -95,13 +95,13 @@ static void pass_ses(const sc_handle* h, const PassParams& pp, const double* U,
         const double A = exp(lp - pp.shift), B = exp(lm - pp.shift);
         const double c = nrm > 0.0 ? (A - B) / (kSqrt2 * nrm) : 0.0;
         T += A + B;
-        Lin = fma(c, l, Lin);
+        K = fma(c, a, K);
         Rad = fma(g, A + B, Rad);
         M = fmax(M, lp);
         Wd = fmax(Wd, (fabs(al - g) + sqrt(w2)) * kInvSqrt2);
         for (int j = 0; j < d; ++j) Sd[j] = fma(c, df[j], Sd[j]);
     }
-    red[kS_T] = T; red[kS_Lin] = Lin; red[kS_Rad] = Rad; red[kS_M] = M;
+    red[kS_T] = T; red[kS_Lin] = K; red[kS_Rad] = Rad; red[kS_M] = M;
     red[kS_F] = F; red[kS_Wd] = Wd; red[kS_Fw] = Fw;
     for (int j = 0; j < d; ++j) red[kS_Vec + j] = Sd[j];
 }
