@@ -978,8 +978,8 @@ static __device__ __noinline__ void rank_exchange(const KParams& p, const RankGr
 // chunks of the warp-partial scratch (pws doubles per warp).  The order is fixed and the
 // same in every CTA, so all CTAs hold identical reduced vectors.
 template <int KIND>
-static __device__ __noinline__ void fold_redundant(const KParams& p, const SmemMap& m,
-                                                   const double* part, int pws) {
+static __device__ __noinline__ void fold_redundant(const KParams& p, double* wpart,
+                                                   double* red, const double* part, int pws) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q0 = warp * p.G / kNW, q1 = (warp + 1) * p.G / kNW;
     for (int c0 = 0; c0 < p.rw; c0 += pws) {
@@ -990,14 +990,14 @@ static __device__ __noinline__ void fold_redundant(const KParams& p, const SmemM
 #pragma unroll 8
             for (int q = q0; q < q1; ++q)
                 acc = op_apply(op, acc, __ldcg(part + (size_t)q * p.rw + j));
-            m.wpart[warp * pws + (j - c0)] = acc;
+            wpart[warp * pws + (j - c0)] = acc;
         }
         consumer_sync();
         for (int j = c0 + (int)threadIdx.x; j < c1; j += kNW * 32) {
             const int op = red_op(KIND, j);
             double acc = op_identity(op);
-            for (int w = 0; w < kNW; ++w) acc = op_apply(op, acc, m.wpart[w * pws + (j - c0)]);
-            m.red[j] = acc;
+            for (int w = 0; w < kNW; ++w) acc = op_apply(op, acc, wpart[w * pws + (j - c0)]);
+            red[j] = acc;
         }
         consumer_sync();
     }
@@ -1038,26 +1038,29 @@ static __device__ __noinline__ void fold_all(const KParams& p, const double* par
 // --------------------------------------------------------------------------------------
 // control tails (warp 0 of every CTA, between passes).  Out of line: the control state is
 // loaded from and stored back to shared memory here, so none of it is live in the
-// streaming loop's register allocation.
+// streaming loop's register allocation.  They take plain pointers, not the SmemMap: a
+// reference would force the map into local memory, and the streaming loop's shared
+// loads would lose their address space (generic LD/ST instead of LDS/STS).
 template <int KIND>
-static __device__ __noinline__ int ctl_tail(const KParams& p, const SmemMap& m,
+static __device__ __noinline__ int ctl_tail(const KParams& p, void* ctl_mem, const double* red,
                                             double* y_tilde, PassParams* pp) {
-    Control<WarpLanes>* const sm = reinterpret_cast<Control<WarpLanes>*>(m.ctl);
+    Control<WarpLanes>* const sm = reinterpret_cast<Control<WarpLanes>*>(ctl_mem);
     Control<WarpLanes> ctl = *sm;
-    const int act = ctl.after_pass(m.red, p.red0, y_tilde, pp);
+    const int act = ctl.after_pass(red, p.red0, y_tilde, pp);
     __syncwarp();
     if ((threadIdx.x & 31) == 0) *sm = ctl;
     __syncwarp();
     return act;
 }
 template <int KIND>
-static __device__ __noinline__ int solve_tail(const KParams& p, const SmemMap& m,
-                                              double* y_tilde, PassParams* pp) {
-    Control<WarpLanes>* const csm = reinterpret_cast<Control<WarpLanes>*>(m.ctl);
-    Search<WarpLanes>* const ssm = reinterpret_cast<Search<WarpLanes>*>(m.srch);
+static __device__ __noinline__ int solve_tail(const KParams& p, void* ctl_mem, void* srch_mem,
+                                              const double* red, double* y_tilde,
+                                              PassParams* pp) {
+    Control<WarpLanes>* const csm = reinterpret_cast<Control<WarpLanes>*>(ctl_mem);
+    Search<WarpLanes>* const ssm = reinterpret_cast<Search<WarpLanes>*>(srch_mem);
     Control<WarpLanes> ctl = *csm;
     Search<WarpLanes> srch = *ssm;
-    const int act = srch.after_pass(ctl, m.red, p.red0, y_tilde, pp);
+    const int act = srch.after_pass(ctl, red, p.red0, y_tilde, pp);
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
         *csm = ctl;
@@ -1293,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             // run at most one pass ahead of the slowest reader
             grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G);
             SCMWU_TMARK(3)
-            fold_redundant<KIND>(p, m, part, pws);
+            fold_redundant<KIND>(p, m.wpart, m.red, part, pws);
             SCMWU_TMARK(4)
             SCMWU_TMARK(6)
         } else {
@@ -1364,8 +1367,8 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
             break;
         }
         if (warp == 0) {
-            const int act = p.solve ? solve_tail<KIND>(p, m, y_tilde, pp)
-                                    : ctl_tail<KIND>(p, m, y_tilde, pp);
+            const int act = p.solve ? solve_tail<KIND>(p, m.ctl, m.srch, m.red, y_tilde, pp)
+                                    : ctl_tail<KIND>(p, m.ctl, m.red, y_tilde, pp);
             if (lane == 0) pp->action = act;
             stream_flush(p, m, r0, r1, warp, ws);
         }

@@ -106,6 +106,30 @@ def _recorded_ses_solve(n, engine, monkeypatch):
     return inst, dev, rep, sol, calls
 
 
+def _classes(steps, ref_eps=1e-3):
+    """Outcome class of every search step: bracketing steps keep (iterations, reason);
+    a refine round (R/meta.py:732-763) is 'separated', 'full' (ran its whole horizon,
+    min(2048 * 4^k, 131072, T_i)) or 'stall' (stopped early by the stall or target rule)."""
+    out, k = [], 0
+    for it, reason, eps, bound in steps:
+        if eps != ref_eps:
+            out.append((it, reason))
+            continue
+        horizon = min(2048 * 4 ** k, 131072, bound)
+        k += 1
+        out.append("separated" if reason == "separated" else
+                   "full" if it >= horizon else "stall")
+    return out
+
+
+def _mine_cls(rep):
+    return _classes([(s.iterations, s.reason, s.eps, s.iteration_bound) for s in rep.steps])
+
+
+def _ref_cls(rec):
+    return _classes([(s[3], s[5], s[1], s[2]) for s in rec["solve"]["search"]])
+
+
 @pytest.mark.parametrize("n", sorted(n for k, n in GROUPS if k == "ses"))
 def test_ses_headline_within_reference(cuda_engine, n, monkeypatch):
     refs = GROUPS[("ses", n)]
@@ -116,47 +140,41 @@ def test_ses_headline_within_reference(cuda_engine, n, monkeypatch):
     assert rep.primal_value <= sol.radius
     terms = {g["solve"]["termination"] for g in refs}
     assert rep.termination.value in terms
-    ref_steps = [_ref_steps(g) for g in refs]
-    mine = _steps(rep)
-    if any(mine == r for r in ref_steps):
-        # the same decisions as (one of) the reference's own runs: the radius agrees to
-        # the drift the reference shows against itself
-        radii = [g["solve"]["radius"] for g in refs]
-        lo, hi = min(radii), max(radii)
-        drift = 0.0
-        for g in refs[1:]:
-            for a, b in zip(refs[0]["solve"]["search"], g["solve"]["search"]):
-                drift = max(drift, abs(a[0] - b[0]) / abs(a[0]))
-        tol = max((hi - lo) / lo, drift, 1e-5)
-        mid = 0.5 * (lo + hi)
-        assert abs(sol.radius - mid) / mid <= tol, (sol.radius, radii, tol)
+    ref_cls = [_ref_cls(g) for g in refs]
+    radii = [g["solve"]["radius"] for g in refs]
+    mid = 0.5 * (min(radii) + max(radii))
+    if _steps(rep) in [_ref_steps(g) for g in refs]:
+        # the reference's own decisions, iteration for iteration
+        assert abs(sol.radius - mid) / mid <= max((max(radii) - min(radii)) / mid, 1e-5)
         return
-    # The trajectory is chaotic (SURVEY finding 5): the first step whose outcome differs
-    # must be a refine round whose outcome flips under 1e-12 perturbations of its level,
-    # with the reference's outcome the typical one.  Everything before it must agree.
-    # (The perturbation runs need the round's arguments: the host-driven search records
+    if _mine_cls(rep) in ref_cls:
+        # the same decisions; refine rounds stop at chaotic points of the trajectory
+        assert abs(sol.radius - mid) / mid <= 1e-4, (sol.radius, radii)
+        return
+    # The trajectory is chaotic (SURVEY finding 5): the first step whose outcome class
+    # differs must be a refine round, every earlier step must agree, and re-running that
+    # round at levels perturbed by 1e-12 relative must give the reference's class in most
+    # of 8 runs.  (The re-runs need the round's arguments: the host-driven search records
     # them; its decisions are the resident search's up to the seed's last bit.)
     _, dev, rep2, _, calls = _recorded_ses_solve(n, cuda_engine, monkeypatch)
-    mine = _steps(rep2)
-    if any(mine == r for r in ref_steps):
+    mine = _mine_cls(rep2)
+    if mine in ref_cls:
         dev.close()
         return
-    first = next(i for i in range(min(len(mine), min(len(r) for r in ref_steps)))
-                 if all(mine[i] != r[i] for r in ref_steps))
-    assert all(any(mine[i] == r[i] for r in ref_steps) for i in range(first))
-    assert rep2.steps[first].eps == 1e-3, "the first difference must be a refine round"
+    first = next(i for i in range(min(len(mine), min(len(r) for r in ref_cls)))
+                 if all(mine[i] != r[i] for r in ref_cls))
+    assert all(any(mine[i] == r[i] for r in ref_cls) for i in range(first))
+    assert isinstance(mine[first], str), "the first difference must be a refine round"
     n_bracket = len(mine) - len(calls)
     oracle, alpha, horizon, stopping, progress, gain_rel, bounds, target, r0 = \
         calls[first - n_bracket]
-    assert r0.iterations == mine[first][0]
-    want = {r[first] for r in ref_steps}
+    want = {r[first] for r in ref_cls}
     hits = 0
     for da in (1e-12, -1e-12, 2e-12, -2e-12, 3e-12, -3e-12, 5e-12, -5e-12):
         r = meta.refine_run(oracle, alpha * (1.0 + da), horizon, stopping, progress,
                             gain_rel=gain_rel, bounds=bounds, target=target)
-        reason = getattr(r, "reason", "separated")
-        hits += (r.iterations, reason) in want or (reason == "refined" and
-                                                   r.iterations == horizon and
-                                                   any(w[0] == horizon for w in want))
+        cls = ("separated" if isinstance(r, meta.PrimalCertificate) else
+               "full" if r.iterations >= horizon else "stall")
+        hits += cls in want
     dev.close()
     assert hits >= 5, (first, mine[first], want, hits)

@@ -5,4 +5,5 @@ for lib in "$@"; do
   SCMWU_LIB=ab/$lib.so python tools/gen_perf.py ses 10000000 100 --horizon 256 --reps 2 2>&1 | grep -v "^generate"
   SCMWU_LIB=ab/$lib.so python tools/gen_perf.py ses 1000000 100 --horizon 1024 --reps 2 2>&1 | grep -v "^generate"
   SCMWU_LIB=ab/$lib.so python tools/gen_perf.py svm 5000000 100 --horizon 256 --reps 2 2>&1 | grep -v "^generate"
+  SCMWU_LIB=ab/$lib.so python tools/gen_perf.py svm 500000 100 --horizon 1024 --reps 2 2>&1 | grep -v "^generate"
 done; done
