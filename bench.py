@@ -407,6 +407,31 @@ def _shared_instance(w, rank, comm):
     return instances.load(path)
 
 
+def exchange_latency_us(w, world, reps=200):
+    """Latency of the per-pass exchange payload (the reduced pass vector: d+7 doubles SES,
+    2d+12 SVM; 864 B / 8.3 KB at d = 100 / 512) as an NCCL all-gather over this node's
+    NVLink, CUDA-event timed on the current stream, max over ranks.  It feeds the
+    HBM+NVLink roofline of a sharded run."""
+    import torch
+    import torch.distributed as tdist
+    rw = w["d"] + 7 if w["kind"] == "ses" else 2 * w["d"] + 12
+    x = torch.zeros(rw, dtype=torch.float64, device="cuda")
+    out = torch.empty(world * rw, dtype=torch.float64, device="cuda")
+    for _ in range(20):
+        tdist.all_gather_into_tensor(out, x)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        tdist.all_gather_into_tensor(out, x)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], device="cuda")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item()), rw * 8
+
+
 def our_arm(args, w, rank, world):
     import torch
     from paper_2405_09157_b200 import ses, svm
@@ -493,6 +518,16 @@ def our_arm(args, w, rank, world):
     bpp = alg_bytes_per_pass(w) // world
     achieved = passes * bpp / kernel_s / 1e9 if kernel_s > 0 else 0.0
     rep0, sol0 = reports[-1]
+    nvl = None
+    if dist:
+        # HBM+NVLink roofline: every pass streams this rank's rows at the HBM peak and
+        # pays one exchange of the pass vector
+        t_x, xbytes = exchange_latency_us(w, world)
+        per_step = passes / len(reports)
+        ideal = per_step * (bpp / (peak * 1e9) + t_x * 1e-6)
+        nvl = {"exchange_bytes": xbytes, "t_exchange_us": t_x,
+               "measured": "NCCL all-gather of the pass vector, CUDA events, max over ranks",
+               "ideal_s_per_step": ideal, "frac": ideal / t_step if t_step > 0 else None}
     iters = [r.total_iterations for r, _ in reports]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
@@ -535,6 +570,8 @@ def our_arm(args, w, rank, world):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
+    if nvl is not None:
+        line["roofline"]["hbm_nvlink"] = nvl
     if rank == 0 and not args.no_cpu_baseline:
         spi, desc, kind = cpu_scaled(w, args.cpu_seconds)
         counts = reference_counts(w)

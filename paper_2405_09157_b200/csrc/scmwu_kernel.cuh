@@ -1341,12 +1341,15 @@ __global__ void __launch_bounds__(kThreads, 1) scmwu_kernel(const __grid_constan
                             ((size_t)((p.pass_base + pass_idx) & 1) * grp.W + grp.rank) * p.rw + j;
                         SC_DCHECK(grp.W <= kMaxWorld && grp.rank < grp.W);
                         for (int r = 0; r < grp.W; ++r) p.mbox[r][off] = acc;
-                        __threadfence_system();
                     } else {
                         p.redg[j] = acc;
                     }
                 }
             }
+            // one system-scope fence per warp after all its mailbox stores (a fence per
+            // column cost ~7 us per pass with 8 emulated ranks at d = 512,
+            // tools/exchange_bench.py)
+            if (kMultiGpu && grp.W > 1 && lane == 0 && c0 + warp < c1) __threadfence_system();
             SCMWU_TMARK(4)
             grid_barrier(grp.bar, (++nbar) * (unsigned long long)grp.G, abort_w, m.flags);
             SCMWU_TMARK(5)
