@@ -114,11 +114,12 @@ def test_bad_arguments_rejected(emu_engine):
 
 
 def test_integration_doc_binding_matches_header():
-    """The ctypes structs a reference maintainer would copy from INTEGRATION.md must have
-    exactly the fields of the package binding (itself checked against the header)."""
+    """The ctypes structs of the reference-side binding (integration/_b200.py, the module
+    INTEGRATION.md §2 drops into symcone/) must have exactly the fields of the package
+    binding (itself checked against the header)."""
     import re
-    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
-    block = doc[doc.index("class Problem(ctypes.Structure)"):doc.index("_lib.sc_create.argtypes")]
+    doc = open(os.path.join(ROOT, "integration", "_b200.py")).read()
+    block = doc[doc.index("class Problem(ctypes.Structure)"):doc.index("def enabled")]
     for cls, ours in (("Problem", nat.ScProblem), ("Args", nat.ScFtpArgs),
                       ("Result", nat.ScFtpResult)):
         body = block[block.index(f"class {cls}("):]
