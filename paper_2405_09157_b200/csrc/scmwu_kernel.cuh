@@ -596,6 +596,18 @@ __device__ __forceinline__ void stream_drain(const KParams& p, const SmemMap& m,
 }
 
 // --------------------------------------------------------------------------------------
+// Which row of a 4-row group a lane group reads.  A 64-bit shared load serves 16 lanes per
+// wavefront: lane groups 0 and 1 (and 2, 3) share one.  With 800-byte rows (d = 100)
+// adjacent rows start 8 banks apart, so groups reading rows r and r + 1 collide on 8 banks
+// (round-1 ncu: 4.2 wavefronts per load instead of 2); rows r and r + 2 start 16 banks
+// apart and do not.  Groups therefore take rows {0, 2, 1, 3}.
+template <int RPW>
+__host__ __device__ __forceinline__ int row_of_group(int grp) {
+    if (RPW != 4) return grp;
+    return grp == 1 ? 2 : (grp == 2 ? 1 : grp);
+}
+
+// --------------------------------------------------------------------------------------
 // batched row math: NB row-groups of RPW rows are reduced by a shuffle reduce-scatter,
 // after which lane (grp, l) holds the complete sums of row (l / DUP) * RPW + grp
 // (DUP = LPR / NB identical copies), so the per-row scalar math (sqrt, exp, div) runs
@@ -639,6 +651,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
     constexpr int NV = 1 + (WIDTH ? 1 : 0) + (CHECK ? 1 : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
+    const int rg = row_of_group<RPW>(grp);
     const int d = p.d, ld = p.ld, dd8 = dd8_of(p.dd);
     const double* ysum = m.vec;
     const double* yprev = m.vec + dd8;
@@ -669,7 +682,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         const int nr = (int)(min(r1, a + (int64_t)p.tile_rows) - a);
         const double* xs = reinterpret_cast<const double*>(st);
         const double* rs = reinterpret_cast<const double*>(st + p.rad_off) + (a & 1);
-        const int r = myk * RPW + grp;              // the row this lane finishes (phase B)
+        const int r = myk * RPW + rg;               // the row this lane finishes (phase B)
         const double g = r < nr ? rs[r] : 0.0;
         // phase A: per-lane partial sums of NB rows; the differences stay in registers
         // for phase C (one shared-memory read and one DFMA less per element)
@@ -677,7 +690,7 @@ __device__ void ses_pass(const KParams& p, const SmemMap& m, const PassParams& p
         double dfk[NB][CPL];
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            const int r = (k ^ myk) * RPW + grp;   // slot k: row-group k ^ myk
+            const int r = (k ^ myk) * RPW + rg;    // slot k: row-group k ^ myk
             const double* xr = xs + (size_t)(r < nr ? r : 0) * ld + l;
             double sa = 0, sw = 0, sf = 0;
 #pragma unroll
@@ -771,6 +784,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
     constexpr int NV = CHECK ? 4 : 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int grp = lane / LPR, l = lane % LPR;
+    const int rg = row_of_group<RPW>(grp);
     const int d = p.d, ld = p.ld, dd8 = dd8_of(p.dd);
     const double* ysum = m.vec;
     const double* yprev = m.vec + dd8;
@@ -804,7 +818,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
         double xk[NB][CPL];   // the staged rows, kept in registers for the G update
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
-            const int r = (k ^ myk) * RPW + grp;   // slot k: row-group k ^ myk
+            const int r = (k ^ myk) * RPW + rg;    // slot k: row-group k ^ myk
             const double* xr = xs + (size_t)(r < nr ? r : 0) * ld + l;
             double dW = 0, dw = 0, dy = 0, dz = 0;
 #pragma unroll
@@ -829,7 +843,7 @@ __device__ void svm_pass(const KParams& p, const SmemMap& m, const PassParams& p
         // is in flight during phases B and C (C3 shape 126.0 -> 125.5 us/pass)
         release_stage(p, m, r0, r1, warp, ws);
         reduce_scatter<LPR, NB, NV>(v, l);
-        const int r = myk * RPW + grp;
+        const int r = myk * RPW + rg;
         double e = 0.0;
         if (r < nr) {
             const double dW = v[0][0];
