@@ -206,6 +206,15 @@ def cpu_sample(w, inst, max_seconds=20.0, max_iters=100_000):
 REF_ROOT = os.path.join(ROOT, "baseline", "_ref")
 
 
+def _ref_cores(w):
+    """Host threads the reference's CPU path uses: SES is numpy element-wise work plus numba
+    loops (one thread); SVM's GEMVs run on OpenBLAS's default thread count."""
+    if w["kind"] == "ses":
+        return 1
+    threads_env = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
+    return int(threads_env) if threads_env else (os.cpu_count() or 1)
+
+
 def reference_counts(w):
     """The reference's own iteration count for the workload's family (same kind, d, eps,
     distribution), from the largest recorded solve in tests/golden/headline/ (recorded by
@@ -357,10 +366,7 @@ def reference_arm(args, w, rank):
         value = alg_bytes_per_pass(w) / spi / 1e9
         metric, unit, hib = "per-iteration HBM GB/s", "GB/s", True
     rows = ws["n"] if w["kind"] == "ses" else ws["n1"] + ws["n2"]
-    threads_env = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS")
-    cores = int(threads_env) if threads_env else (os.cpu_count() or 1)
-    if w["kind"] == "ses":
-        cores = 1   # numpy element-wise + numba loops: one thread
+    cores = _ref_cores(w)
     desc = (f"{got} MWU iterations per step (one refine_run of the "
             f"{'unmodified reference, baseline/_ref' if use_ref else 'oracle port'}) on a "
             f"{rows}-row sample of the workload's distribution, {spi / factor:.4f} s/iter "
@@ -579,7 +585,7 @@ def our_arm(args, w, rank, world):
                                  f"at n={counts[1]})") if counts else
                      (rep0.total_iterations, "the GPU solve's count"))
         line["cpu_baseline"] = {
-            "value": spi * its, "unit": "s", "cores": 1, "kind": kind,
+            "value": spi * its, "unit": "s", "cores": _ref_cores(w), "kind": kind,
             "sample": f"{desc}; x {its} iterations = {note}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -730,7 +736,7 @@ def gen_arm(args, w, rank, world):
         its = counts[0] if counts else iters
         cv = bpp / spi / 1e9 if fixed else spi * its
         line["cpu_baseline"] = {
-            "value": cv, "unit": unit, "cores": 1, "kind": kind,
+            "value": cv, "unit": unit, "cores": _ref_cores(w), "kind": kind,
             "sample": desc + ("; GB/s = algorithmic bytes / s" if fixed else
                               f"; x {its} iterations = " +
                               (f"the reference's own count for this family (recorded solve "
