@@ -1,8 +1,8 @@
-"""Where the non-kernel wall time of one C2 solve goes (dev tool): every native call
-made by solve_ses (sc_ftp, sc_progress, ...) is timed on the host; prints per call
-wall vs kernel time and the host gaps between calls.
+"""Where the non-kernel wall time of one solve goes (dev tool): every native call made
+by solve_ses / solve_svm (sc_create, sc_solve or sc_ftp, sc_progress, sc_pd_pair, ...) is
+timed on the host; prints per call wall vs kernel time and the host gaps between calls.
 
-    python tools/solve_gaps.py [--reps 3] [--resident]
+    python tools/solve_gaps.py [--reps 3] [--resident] [--workload ses_c2|svm_c3|...]
 """
 import os
 import sys
@@ -22,15 +22,16 @@ def wrap(name):
         t0 = time.perf_counter()
         out = fn(self, *a, **k)
         t1 = time.perf_counter()
-        LOG.append((name, t0, t1, getattr(out, "kernel_ms", 0.0) / 1e3,
-                    getattr(out, "passes", 0)))
+        res = out[1] if isinstance(out, tuple) and len(out) == 4 else out   # sc_solve
+        LOG.append((name, t0, t1, getattr(res, "kernel_ms", 0.0) / 1e3,
+                    getattr(res, "passes", 0)))
         return out
     setattr(nat.Handle, name, timed)
 
 
 def main():
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 3
-    for name in ("ftp", "progress", "iterate", "pd_pair", "close", "set_range"):
+    for name in ("ftp", "solve", "progress", "iterate", "pd_pair", "close", "set_range"):
         wrap(name)
     create = nat.Engine.create
 
@@ -48,13 +49,17 @@ def main():
         LOG.append(("range", t0, time.perf_counter(), 0.0, 0))
         return out
     ses.ses_range = timed_range
-    w = bench.WORKLOADS["ses_c2"]
+    wl = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else "ses_c2"
+    w = bench.WORKLOADS[wl]
     inst = bench.make_instance(w, pinned=True)
-    dev = ses.ses_device(inst) if "--resident" in sys.argv else None
+    from paper_2405_09157_b200 import svm
+    dev = None
+    if "--resident" in sys.argv:
+        dev = ses.ses_device(inst) if w["kind"] == "ses" else svm.svm_device(inst)
     for rep in range(reps):
         LOG.clear()
         t0 = time.perf_counter()
-        r, _ = ses.solve_ses(inst, w["eps"], device=dev)
+        r, _ = bench.solve(w, inst, dev)
         t1 = time.perf_counter()
         calls = sum(c[2] - c[1] for c in LOG)
         kern = sum(c[3] for c in LOG)
