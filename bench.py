@@ -336,6 +336,13 @@ def reference_arm(args, w, rank):
     ws, factor = _sample_rows(w)
     inst = make_instance(ws)
     use_ref = _import_reference() is not None
+    if use_ref:
+        try:                     # the reference runs here (numba JIT included), or the port
+            ref_sample(ws, inst, 1)
+        except Exception as exc:  # noqa: BLE001
+            print(f"bench: the reference failed on this host ({exc}); timing the oracle port",
+                  file=sys.stderr)
+            use_ref = False
     kind = "reference" if use_ref else "port"
     fixed = w.get("horizon") is not None   # per-iteration GB/s workloads (C5 shape)
     counts = reference_counts(w)
@@ -755,8 +762,15 @@ def cpu_scaled(w, seconds):
     ws, factor = _sample_rows(w)
     inst = make_instance(ws)
     rows = ws["n"] if w["kind"] == "ses" else ws["n1"] + ws["n2"]
-    if _import_reference() is not None:
-        ref_sample(ws, inst, 1)                  # numba JIT of the reference
+    use_ref = _import_reference() is not None
+    if use_ref:
+        try:
+            ref_sample(ws, inst, 1)              # numba JIT of the reference
+        except Exception as exc:  # noqa: BLE001
+            print(f"bench: the reference failed on this host ({exc}); timing the oracle port",
+                  file=sys.stderr)
+            use_ref = False
+    if use_ref:
         spi0, _, _ = ref_sample(ws, inst, 1)
         k = max(1, int(seconds / max(spi0, 1e-9)))
         spi, its, _ = ref_sample(ws, inst, k)
