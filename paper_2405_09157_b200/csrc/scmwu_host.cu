@@ -813,6 +813,8 @@ static int fill_params(sc_handle* h, KParams& p, long long* slot_cycles) {
         cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, h->prob.device);
         p.xtimeout = (long long)(secs * 1e3 * (double)(khz > 0 ? khz : 2000000));
     }
+    p.drop_rank = -1;
+    if (const char* e = getenv("SCMWU_FAULT_DROP_RANK")) p.drop_rank = atoi(e);
     if (h->vworld > 1) {
         for (int r = 0; r < h->vworld; ++r) {
             p.mflag[r] = reinterpret_cast<unsigned long long*>(h->peer_base[r]);

@@ -198,6 +198,7 @@ struct KParams {
     double* mbox[kMaxWorld];   // rank r's mailbox data [2][world][rw] (peer pointers)
     unsigned long long* mflag[kMaxWorld];   // rank r's arrival flags [world]
     long long xtimeout;        // cycles a rank waits for a peer's exchange flag
+    int drop_rank;             // tests only (SCMWU_FAULT_DROP_RANK): this rank never arrives
     // whole-solve residency (sc_solve): the adaptive search runs between the passes
     int solve;
     sc_solve_args sargs;
@@ -954,7 +955,8 @@ static __device__ __noinline__ void rank_exchange(const KParams& p, const RankGr
     // (one thread doing them in sequence cost one system-scope round trip per rank).
     // Ordering: the mailbox stores of every folding warp precede the grid barrier this
     // CTA passed (thread 0's acquire + bar.sync), so thread r's release covers them.
-    if (tid < g.W && (int)blockIdx.x == g.first)
+    // (fault injection for the failure-path test: rank p.drop_rank never raises its flags)
+    if (tid < g.W && (int)blockIdx.x == g.first && g.rank != p.drop_rank)
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p.mflag[tid] + g.rank),
                      "l"(want)
                      : "memory");
