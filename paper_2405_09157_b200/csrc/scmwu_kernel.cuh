@@ -1075,6 +1075,27 @@ static __device__ __noinline__ int solve_tail(const KParams& p, void* ctl_mem, v
     Control<WarpLanes>* const csm = reinterpret_cast<Control<WarpLanes>*>(ctl_mem);
     Search<WarpLanes>* const ssm = reinterpret_cast<Search<WarpLanes>*>(srch_mem);
     Control<WarpLanes> ctl = *csm;
+    const int phase = ssm->phase;
+    if (phase == kBracket || phase == kRefine) {
+        // inside a feasibility test (almost every pass): only the test's control state is
+        // needed; the search state is loaded when the test ends
+        int act = ctl.after_pass(red, p.red0, y_tilde, pp);
+        if (act == kPass) {
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) *csm = ctl;
+            __syncwarp();
+            return act;
+        }
+        Search<WarpLanes> srch = *ssm;
+        act = srch.test_done(ctl, p.red0, y_tilde, pp);
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+            *csm = ctl;
+            *ssm = srch;
+        }
+        __syncwarp();
+        return act;
+    }
     Search<WarpLanes> srch = *ssm;
     const int act = srch.after_pass(ctl, red, p.red0, y_tilde, pp);
     __syncwarp();
