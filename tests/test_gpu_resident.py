@@ -63,3 +63,24 @@ def test_ses_resident_search_certified(monkeypatch, args, eps):
         assert r.primal_value <= s.radius
     assert r1.termination == r2.termination
     assert abs(s1.radius - s2.radius) <= 3 * eps * s1.radius
+
+
+@pytest.mark.parametrize("cfg", [dict(iteration_cap_override=64), dict(early_stop=False),
+                                 dict(delta=1e-3, patience=3)])
+def test_svm_resident_search_configs(monkeypatch, cfg):
+    """RunConfig knobs reach the device search: an iteration cap, early stop off, other
+    delta / patience — the same decisions as the host-driven search."""
+    from paper_2405_09157_b200 import RunConfig
+    inst, _ = instances.gen_svm(500, 600, 12, 3, 0.7)
+    c = RunConfig(**cfg)
+    (r1, s1), (r2, s2) = _both(monkeypatch, lambda: svm.solve_svm(inst, 1e-2, c))
+    assert _steps(r1) == _steps(r2) and r1.termination == r2.termination
+    assert math.isclose(s1.margin, s2.margin, rel_tol=1e-12)
+
+
+def test_resident_search_tiny_instances():
+    """Smallest shapes through sc_solve: the SPEC two-point SVM and collinear SES."""
+    r, s = svm.solve_svm(svm.SvmInstance(np.array([[1.0, 0.0]]), np.array([[-1.0, 0.0]])), 0.01)
+    assert s.margin == 2.0 and s.pd_distance == 2.0
+    r, s = ses.solve_ses(ses.SesInstance(np.array([[0.0], [1.0], [2.0]]), np.zeros(3)), 0.05)
+    assert 1.0 <= s.radius <= 1.05
