@@ -84,3 +84,23 @@ def test_resident_search_tiny_instances():
     assert s.margin == 2.0 and s.pd_distance == 2.0
     r, s = ses.solve_ses(ses.SesInstance(np.array([[0.0], [1.0], [2.0]]), np.zeros(3)), 0.05)
     assert 1.0 <= s.radius <= 1.05
+
+
+@pytest.mark.parametrize("n1,n2,d,seed,gap", [(60, 70, 1, 1, 0.8), (40, 90, 3, 2, 0.5),
+                                              (60, 70, 33, 5, 0.8), (60, 70, 129, 5, 0.8),
+                                              (50, 45, 257, 6, 1.0), (60, 70, 512, 5, 0.8)])
+def test_svm_full_solve_matches_oracle_across_d(n1, n2, d, seed, gap):
+    """The whole device solve (sc_solve) vs the oracle's restatement of the reference's
+    solve_svm (bit-exact with the reference) across the kernel configurations (lanes per
+    row 2..32, odd d with padded rows, d = 512): identical search steps, iteration counts
+    and termination; margin and pd distance to 1e-6 (SVM decisions are robust)."""
+    import oracle as O
+    inst, _ = instances.gen_svm(n1, n2, d, seed, gap)
+    rep, sol = svm.solve_svm(inst, 1e-2)
+    ref = O.solve_svm(inst.P, inst.Q, 1e-2)
+    assert rep.total_iterations == ref["iterations"] and rep.search_steps == ref["steps"]
+    assert rep.termination.value == ref["termination"]
+    assert [(s.iterations, s.reason) for s in rep.steps] == \
+        [(s.iterations, s.reason) for s in ref["search"]]
+    assert math.isclose(sol.margin, ref["margin"], rel_tol=1e-6)
+    assert math.isclose(sol.pd_distance, ref["pd_distance"], rel_tol=1e-6)
