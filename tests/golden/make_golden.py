@@ -11,6 +11,8 @@ it writes under tests/golden/ are committed and are what the tests read.
     python tests/golden/make_golden.py headline KIND N THREADS
         # one headline-regime solve (eps=1e-3, d=100: SES uniform-ball / SVM gap 1)
         # with its per-call records -> tests/golden/headline/KIND_nN_tTHREADS.json
+    python tests/golden/make_golden.py family KIND EPS THREADS ARGS...
+        # the same for another instance family (ses: n d seed dist; svm: n1 n2 d seed gap)
 
 Instances are NOT stored: tests regenerate them from (n, d, seed, dist) with
 paper_2405_09157_b200.instances, whose bit-exactness against the reference
@@ -383,18 +385,18 @@ def gen_baselines():
 # BASELINE configs[1..4] run at eps=1e-3, d=100 (SES uniform-ball, SVM gap 1); these
 # record the reference's own solves of the same families at sizes it finishes in
 # minutes to hours, so the device's refine/stop behaviour can be compared with it.
-def gen_headline(kind: str, n: int, threads: int):
-    eps = 1e-3
+def gen_headline(kind: str, n: int, threads: int, args=None, eps: float = 1e-3,
+                 name: str | None = None):
     t0 = time.time()
     cfg = RunConfig(eps=eps, threads=threads)
     if kind == "ses":
-        args = (n, 100, 0, "uniform-ball")
+        args = tuple(args) if args is not None else (n, 100, 0, "uniform-ball")
         inst = instances.gen_ses(*args)
         (r, s), calls = record_calls(lambda: ses.solve_ses(inst, eps, cfg))
         rec = _solve_ses_rec(r, s)
         D, _, _ = ses.ses_range(inst)
     else:
-        args = (n // 2, n - n // 2, 100, 0, 1.0)
+        args = tuple(args) if args is not None else (n // 2, n - n // 2, 100, 0, 1.0)
         inst, _ = instances.gen_svm(*args)
         (r, s), calls = record_calls(lambda: svm.solve_svm(inst, eps, cfg))
         rec = _solve_svm_rec(r, s)
@@ -407,7 +409,7 @@ def gen_headline(kind: str, n: int, threads: int):
            "wall_s": wall, "D": _f(D), "s_per_iter": wall / max(1, rec["iterations"]),
            "solve": rec, "calls": calls}
     os.makedirs(os.path.join(HERE, "headline"), exist_ok=True)
-    dump(os.path.join("headline", f"{kind}_n{n}_t{threads}.json"), out)
+    dump(os.path.join("headline", name or f"{kind}_n{n}_t{threads}.json"), out)
     print(kind, args, threads, rec["iterations"], rec["termination"], f"{wall:.1f}s",
           file=sys.stderr)
 
@@ -426,5 +428,17 @@ if __name__ == "__main__":
         gen_long()
     elif what == "headline":
         gen_headline(sys.argv[2], int(sys.argv[3]), int(sys.argv[4]))
+    elif what == "family":
+        # family KIND EPS THREADS ARGS...  (ses: n d seed dist; svm: n1 n2 d seed gap)
+        kind, eps, th = sys.argv[2], float(sys.argv[3]), int(sys.argv[4])
+        raw = sys.argv[5:]
+        if kind == "ses":
+            fargs = (int(raw[0]), int(raw[1]), int(raw[2]), raw[3])
+            n = fargs[0]
+        else:
+            fargs = (int(raw[0]), int(raw[1]), int(raw[2]), int(raw[3]), float(raw[4]))
+            n = fargs[0] + fargs[1]
+        tag = "_".join(str(a) for a in fargs)
+        gen_headline(kind, n, th, fargs, eps, f"{kind}_{tag}_e{eps:g}_t{th}.json")
     else:
         raise SystemExit(f"unknown group {what}")

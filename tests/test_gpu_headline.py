@@ -33,11 +33,12 @@ pytestmark = pytest.mark.gpu
 
 
 def _groups():
+    """Recorded reference solves grouped by (kind, instance args, eps); each group holds the
+    reference's runs with different `threads` (reduction partitions)."""
     g = {}
     for f in sorted(glob.glob(os.path.join(GOLDEN, "headline", "*.json"))):
         rec = json.load(open(f))
-        n = rec["inst"][0] if rec["kind"] == "ses" else rec["inst"][0] + rec["inst"][1]
-        g.setdefault((rec["kind"], n), []).append(rec)
+        g.setdefault((rec["kind"], tuple(rec["inst"]), rec["eps"]), []).append(rec)
     return g
 
 
@@ -45,16 +46,24 @@ GROUPS = _groups()
 _solved = {}
 
 
-def _solve(kind, n, engine):
-    key = (kind, n)
+def _solve(key, engine):
     if key not in _solved:
+        kind, args, eps = key
         if kind == "ses":
-            inst = instances.gen_ses(n, 100, 0, "uniform-ball")
-            _solved[key] = (inst,) + ses.solve_ses(inst, 1e-3, engine=engine)
+            inst = instances.gen_ses(*args)
+            _solved[key] = (inst,) + ses.solve_ses(inst, eps, engine=engine)
         else:
-            inst, _ = instances.gen_svm(n // 2, n - n // 2, 100, 0, 1.0)
-            _solved[key] = (inst,) + svm.solve_svm(inst, 1e-3, engine=engine)
+            inst, _ = instances.gen_svm(*args)
+            _solved[key] = (inst,) + svm.solve_svm(inst, eps, engine=engine)
     return _solved[key]
+
+
+def _ids(kind):
+    return sorted((k for k in GROUPS if k[0] == kind), key=lambda k: (k[1], k[2]))
+
+
+def _name(key):
+    return "-".join(str(a) for a in key[1]) + f"-eps{key[2]:g}"
 
 
 def _steps(rep):
@@ -65,10 +74,10 @@ def _ref_steps(rec):
     return [(s[3], s[5]) for s in rec["solve"]["search"]]
 
 
-@pytest.mark.parametrize("n", sorted(n for k, n in GROUPS if k == "svm"))
-def test_svm_headline_matches_reference(cuda_engine, n):
-    refs = GROUPS[("svm", n)]
-    inst, rep, sol = _solve("svm", n, cuda_engine)
+@pytest.mark.parametrize("key", _ids("svm"), ids=_name)
+def test_svm_headline_matches_reference(cuda_engine, key):
+    refs = GROUPS[key]
+    inst, rep, sol = _solve(key, cuda_engine)
     for g in refs:
         s = g["solve"]
         assert rep.total_iterations == s["iterations"]
@@ -86,7 +95,7 @@ def test_svm_headline_matches_reference(cuda_engine, n):
     assert sol.margin <= sol.pd_distance
 
 
-def _recorded_ses_solve(n, engine, monkeypatch):
+def _recorded_ses_solve(key, engine, monkeypatch):
     """The SES solve driven from the host with every feasibility test's arguments
     recorded, so a step can be re-run under perturbations."""
     monkeypatch.setenv("SCMWU_HOST_SEARCH", "1")
@@ -100,9 +109,9 @@ def _recorded_ses_solve(n, engine, monkeypatch):
         return r
 
     monkeypatch.setattr(meta, "refine_run", rec)
-    inst = instances.gen_ses(n, 100, 0, "uniform-ball")
+    inst = instances.gen_ses(*key[1])
     dev = ses.ses_device(inst, engine=engine)
-    rep, sol = ses.solve_ses(inst, 1e-3, device=dev)
+    rep, sol = ses.solve_ses(inst, key[2], device=dev)
     return inst, dev, rep, sol, calls
 
 
@@ -122,18 +131,19 @@ def _classes(steps, ref_eps=1e-3):
     return out
 
 
-def _mine_cls(rep):
-    return _classes([(s.iterations, s.reason, s.eps, s.iteration_bound) for s in rep.steps])
+def _mine_cls(rep, eps):
+    return _classes([(s.iterations, s.reason, s.eps, s.iteration_bound) for s in rep.steps],
+                    eps)
 
 
 def _ref_cls(rec):
-    return _classes([(s[3], s[5], s[1], s[2]) for s in rec["solve"]["search"]])
+    return _classes([(s[3], s[5], s[1], s[2]) for s in rec["solve"]["search"]], rec["eps"])
 
 
-@pytest.mark.parametrize("n", sorted(n for k, n in GROUPS if k == "ses"))
-def test_ses_headline_within_reference(cuda_engine, n, monkeypatch):
-    refs = GROUPS[("ses", n)]
-    inst, rep, sol = _solve("ses", n, cuda_engine)
+@pytest.mark.parametrize("key", _ids("ses"), ids=_name)
+def test_ses_headline_within_reference(cuda_engine, key, monkeypatch):
+    refs = GROUPS[key]
+    inst, rep, sol = _solve(key, cuda_engine)
     # certified: the reported radius covers every ball around the returned centre
     dist = np.sqrt(((inst.centers - sol.center) ** 2).sum(axis=1)) + inst.radii
     assert dist.max() <= sol.radius * (1 + 1e-9)
@@ -147,7 +157,7 @@ def test_ses_headline_within_reference(cuda_engine, n, monkeypatch):
         # the reference's own decisions, iteration for iteration
         assert abs(sol.radius - mid) / mid <= max((max(radii) - min(radii)) / mid, 1e-5)
         return
-    if _mine_cls(rep) in ref_cls:
+    if _mine_cls(rep, key[2]) in ref_cls:
         # the same decisions; refine rounds stop at chaotic points of the trajectory
         assert abs(sol.radius - mid) / mid <= 1e-4, (sol.radius, radii)
         return
@@ -156,8 +166,8 @@ def test_ses_headline_within_reference(cuda_engine, n, monkeypatch):
     # round at levels perturbed by 1e-12 relative must give the reference's class in most
     # of 8 runs.  (The re-runs need the round's arguments: the host-driven search records
     # them; its decisions are the resident search's up to the seed's last bit.)
-    _, dev, rep2, _, calls = _recorded_ses_solve(n, cuda_engine, monkeypatch)
-    mine = _mine_cls(rep2)
+    _, dev, rep2, _, calls = _recorded_ses_solve(key, cuda_engine, monkeypatch)
+    mine = _mine_cls(rep2, key[2])
     if mine in ref_cls:
         dev.close()
         return
