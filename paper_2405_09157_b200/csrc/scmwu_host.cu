@@ -419,7 +419,6 @@ static int configure(sc_handle* h, int grid_req) {
     auto need = [&](int sw) {
         return (size_t)kNW * sw * h->stage_stride + smem_fixed_bytes(h->dd, h->rw, h->pw, kNW * sw);
     };
-    (void)0;
     int S = 1;
     while (S < 64 && need(S + 1) <= (size_t)kMaxSmem) ++S;
     h->resident = per_warp <= S ? 1 : 0;
