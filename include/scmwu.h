@@ -201,6 +201,14 @@ int sc_create_generated(sc_problem* prob, const sc_gen* gen, double* v1_out,
 /* Set the range D; rho, R, rank and ln_r follow as in the solvers (R/ses.py:161,169,
  * R/svm.py:168,186). */
 int sc_set_range(sc_handle* h, double D);
+/* The range D over this handle's resident rows, bit-identical to the reference's numpy
+ * expression: SES max over global rows i >= 1 of |v_i - v_1| + g_1 + g_i (R/ses.py:65-72;
+ * a shard without row 0 needs v_1 and g_1 from sc_set_globals first), SVM max_i |x_i|
+ * (R/svm.py:62-66).  Row norms follow np.linalg.norm's pairwise summation order
+ * (csrc/np_rownorm.h), so sharded callers max-reduce the shards' values and every rank
+ * gets the single-process D; -inf for a shard with no such row.  Replaces the O(nd) host
+ * scan of ses_range / max_norm before sc_set_range. */
+int sc_row_range(sc_handle* h, double* D_out);
 /* Copy `count` resident rows starting at local row `first` to out (count x d, row-major). */
 int sc_read_rows(sc_handle* h, int64_t first, int64_t count, double* out);
 /* Independent verification baselines over a resident single-GPU instance (SURVEY §8(f)

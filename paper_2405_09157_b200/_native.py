@@ -112,7 +112,7 @@ EXPORTS = ("sc_create", "sc_ftp", "sc_progress", "sc_iterate", "sc_pd_commit", "
            "sc_local_red0", "sc_progress_parts", "sc_set_globals", "sc_ipc_handle",
            "sc_connect", "sc_last_error", "sc_destroy", "sc_version", "sc_create_generated",
            "sc_set_range", "sc_read_rows", "sc_meb_baseline", "sc_gilbert_baseline",
-           "sc_pool_trim", "sc_solve")
+           "sc_pool_trim", "sc_solve", "sc_row_range")
 
 _dp = ctypes.POINTER(ctypes.c_double)
 
@@ -165,6 +165,7 @@ class Engine:
         lib.sc_create_generated.argtypes = [ctypes.POINTER(ScProblem), ctypes.POINTER(ScGen),
                                             _dp, ctypes.POINTER(vp)]
         lib.sc_set_range.argtypes = [vp, ctypes.c_double]
+        lib.sc_row_range.argtypes = [vp, _dp]
         lib.sc_read_rows.argtypes = [vp, ctypes.c_int64, ctypes.c_int64, _dp]
         lib.sc_meb_baseline.argtypes = [vp, ctypes.c_int64, _dp, _dp]
         lib.sc_gilbert_baseline.argtypes = [vp, ctypes.c_double, ctypes.c_int64, _dp, _dp,
@@ -348,7 +349,28 @@ class Handle:
 
     def set_range(self, D: float) -> None:
         self._check(self.engine.lib.sc_set_range(self.h, D), "sc_set_range")
-        self.prob.D = D
+        # the constants the library derived (R/ses.py:161,169, R/svm.py:168,186)
+        p = self.prob
+        p.D = D
+        if p.kind == SC_SES:
+            p.rho, p.R, p.rank = 3.0 * D / math.sqrt(2.0), math.sqrt(2.0), 2 * (p.n - 1)
+        else:
+            p.rho, p.R, p.rank = 2.0 * D, 2.0, p.n
+        p.ln_r = math.log(p.rank)
+
+    def row_range(self) -> float:
+        """The reference's range expression over this handle's rows, evaluated on the
+        device in numpy's operation order (sc_row_range): bit-identical to ses_range /
+        max_norm over the same rows; -inf for a shard without such rows."""
+        D = ctypes.c_double()
+        self._check(self.engine.lib.sc_row_range(self.h, ctypes.byref(D)), "sc_row_range")
+        return float(D.value)
+
+    def set_range_from_rows(self) -> float:
+        """D of a single-GPU handle from its resident rows, then sc_set_range."""
+        D = self.row_range()
+        self.set_range(D)
+        return D
 
     def meb_baseline(self, iters: int) -> tuple[np.ndarray, float]:
         c = np.zeros(self.d)

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 
+#include "np_rownorm.h"
 #include "scmwu_handle.h"
 
 namespace scmwu {
@@ -115,7 +116,69 @@ __global__ void gen_kernel(double* X, int ld, int d, int64_t rows, int64_t grow0
     if (dmax && lane == 0 && best > 0.0) atomicMax(dmax, (unsigned long long)__double_as_longlong(best));
 }
 
+// order-preserving integer image of a double (atomicMax over the images = max over the
+// values, independent of the order the rows are visited in)
+__device__ __forceinline__ unsigned long long ord_key(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double ord_value(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    double v;
+    memcpy(&v, &b, 8);
+    return v;
+}
+
+// The range term of rows [first, rows) with numpy's operation order (np_rownorm.h): one
+// thread per row (a one-off pass; the row's sectors are reused from L1 by the thread's
+// next loads).  SES: (|x_i - v1| + g1) + g_i, SVM: |x_i|.
+__global__ void range_kernel(const double* X, int ld, int d, int64_t first, int64_t rows,
+                             const double* radii, const double* anchor, double g1, int ses,
+                             unsigned long long* kmax) {
+    double best = -INFINITY;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = first + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+         i += stride) {
+        const double v = np_range_term(X + i * (int64_t)ld, anchor, d, g1,
+                                       ses ? radii[i] : 0.0, ses != 0);
+        best = v > best || v != v ? v : best;   // NaN propagates, as in numpy's max
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, best, o);
+        best = u > best || u != u ? u : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best != -INFINITY) atomicMax(kmax, ord_key(best));
+}
+
 }  // namespace scmwu
+
+// D of the resident rows, numpy-exact (R/ses.py:65-72 over global rows >= 1 with the
+// anchor v1 and g1 of the handle; R/svm.py:62-66); -inf when this shard has no such row
+int sc_row_range(sc_handle* h, double* D_out) {
+    if (!h || !D_out) return SC_EARG;
+    const sc_problem& P = h->prob;
+    const bool ses = P.kind == SC_SES;
+    const int64_t first = ses && P.row0 == 0 ? 1 : 0;
+    const int64_t rows = P.n_local;
+    CK(cudaSetDevice(P.device), "set device");
+    unsigned long long* kmax = reinterpret_cast<unsigned long long*>(h->scratch);
+    CK(cudaMemsetAsync(kmax, 0, 8, h->stream), "zero range");   // key 0 < key(-inf)
+    if (rows > first) {
+        const int64_t per = 256;
+        const int blocks = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)h->sms * 8, (rows - first + per - 1) / per));
+        range_kernel<<<blocks, (int)per, 0, h->stream>>>(h->X, h->ld, P.d, first, rows,
+                                                         h->radii, ses ? h->v1 : nullptr,
+                                                         h->g1, ses ? 1 : 0, kmax);
+        ++h->launches;
+        CK(cudaGetLastError(), "range kernel");
+    }
+    unsigned long long k = 0;
+    CK(h_get(h, &k, kmax, 8), "read range");
+    *D_out = k == 0 ? -INFINITY : ord_value(k);
+    return SC_OK;
+}
 
 // Draw this handle's rows (and, SES, the anchor row 0) into HBM; *D_out receives the range
 // over this shard's rows (SES max_i |v_1 - v_i|, SVM max_i |x_i|).

@@ -141,14 +141,6 @@ def _connect(h: nat.Handle, comm: Comm, kind: int, d: int, dev: ShardedDevicePro
     emu_hook(h.h, dev._cb)
 
 
-def _rows_max(fn, a: int, b: int) -> float:
-    """max over rows [a, b) of fn(lo, hi) evaluated on 4096-row chunks (per-row norms do
-    not depend on the chunking and max is order-free: bit-identical to one call)."""
-    if b <= a:
-        return -math.inf
-    return max(fn(lo, min(b, lo + 4096)) for lo in range(a, b, 4096))
-
-
 def _global_max(comm: Comm, x: float) -> float:
     return float(np.max(comm.all_gather_array(np.array([x]))))
 
@@ -157,23 +149,20 @@ def ses_device_sharded(inst, comm: Comm, engine: Optional[nat.Engine] = None, de
                        grid: int = 0) -> ShardedDeviceProblem:
     """This rank's share of an SES instance (every rank passes the full instance, e.g. a
     memory map; only this rank's rows are read and uploaded).  The range D is the
-    reference's expression (R/ses.py:65-72) over this rank's rows, max-reduced across ranks
-    (bit-identical to the single-process value)."""
+    reference's expression (R/ses.py:65-72) over this rank's resident rows (sc_row_range,
+    numpy's operation order), max-reduced across ranks: bit-identical to the
+    single-process value."""
     from .ses import ses_cone
     eng = engine if engine is not None else nat.cuda_engine()
     n = inst.n
     r0, r1 = row_ranges(n, comm.world)[comm.rank]
-    c, rad = inst.centers, inst.radii
-    v1 = np.asarray(c[0])
-    D = _global_max(comm, _rows_max(
-        lambda lo, hi: float((np.linalg.norm(c[lo:hi] - v1, axis=1) + rad[0] + rad[lo:hi]).max()),
-        max(r0, 1), r1))
-    h = eng.create(nat.SC_SES, inst.centers[r0:r1], None, inst.radii[r0:r1], D=D,
-                   rho=3.0 * D / SQRT2, R=SQRT2, rank=2 * (n - 1), grid=grid, device=device,
+    h = eng.create(nat.SC_SES, inst.centers[r0:r1], None, inst.radii[r0:r1], D=0.0,
+                   rho=0.0, R=SQRT2, rank=2 * (n - 1), grid=grid, device=device,
                    shard=(comm.world, comm.rank, r0, n))
     ops = red_ops(nat.SC_SES, inst.d)
     h.set_globals(fold_ranks(comm.all_gather_array(h.local_red0()), ops), inst.centers[0],
                   float(inst.radii[0]))
+    h.set_range(_global_max(comm, h.row_range()))   # needs v1 and g1 (set_globals)
     dev = ShardedDeviceProblem(h, ses_cone(n, inst.d), nat.SC_SES, comm)
     _connect(h, comm, nat.SC_SES, inst.d, dev)
     return dev
@@ -186,17 +175,12 @@ def svm_device_sharded(inst, comm: Comm, engine: Optional[nat.Engine] = None, de
     eng = engine if engine is not None else nat.cuda_engine()
     n1, n = inst.n1, inst.n1 + inst.n2
     r0, r1 = row_ranges(n, comm.world)[comm.rank]
-    # max_norm (R/svm.py:62-66) over this rank's rows, max-reduced across ranks
-    P, Q = inst.P, inst.Q
-    D = _global_max(comm, max(
-        _rows_max(lambda lo, hi: float(np.linalg.norm(P[lo:hi], axis=1).max()),
-                  max(r0, 0), min(r1, n1)),
-        _rows_max(lambda lo, hi: float(np.linalg.norm(Q[lo:hi], axis=1).max()),
-                  max(r0 - n1, 0), max(r1 - n1, 0))))
     rows = np.concatenate([inst.P[max(r0, 0):min(r1, n1)],
                            inst.Q[max(r0 - n1, 0):max(r1 - n1, 0)]])
-    h = eng.create(nat.SC_SVM, rows, None, None, D=D, rho=2.0 * D, R=2.0, rank=n, n1=n1,
+    h = eng.create(nat.SC_SVM, rows, None, None, D=0.0, rho=0.0, R=2.0, rank=n, n1=n1,
                    grid=grid, device=device, shard=(comm.world, comm.rank, r0, n))
+    # max_norm (R/svm.py:62-66) over this rank's resident rows, max-reduced across ranks
+    h.set_range(_global_max(comm, h.row_range()))
     ops = red_ops(nat.SC_SVM, inst.d)
     h.set_globals(fold_ranks(comm.all_gather_array(h.local_red0()), ops))
     dev = ShardedDeviceProblem(h, svm_cone(n), nat.SC_SVM, comm)

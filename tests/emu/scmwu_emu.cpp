@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "../../paper_2405_09157_b200/csrc/np_rownorm.h"
 #include "../../paper_2405_09157_b200/csrc/scmwu_control.h"
 
 using namespace scmwu;
@@ -389,7 +390,34 @@ int sc_create_generated(sc_problem*, const sc_gen*, double*, sc_handle** out) {
 
 int sc_set_range(sc_handle* h, double D) {
     if (!h || !(D >= 0.0)) return SC_EARG;
-    h->prob.D = D;
+    sc_problem& p = h->prob;   // as the device library's derive_constants
+    p.D = D;
+    if (p.kind == SC_SES) {
+        p.rho = 3.0 * D / sqrt(2.0);
+        p.R = sqrt(2.0);
+        p.rank = 2 * (p.n - 1);
+    } else {
+        p.rho = 2.0 * D;
+        p.R = 2.0;
+        p.rank = p.n;
+    }
+    p.ln_r = log((double)p.rank);
+    return SC_OK;
+}
+
+// the device's sc_row_range on the host: the same numpy-order row norms (np_rownorm.h)
+int sc_row_range(sc_handle* h, double* D_out) {
+    if (!h || !D_out) return SC_EARG;
+    const sc_problem& P = h->prob;
+    const bool ses = P.kind == SC_SES;
+    const int d = P.d;
+    double best = -INFINITY;
+    for (int64_t i = ses && P.row0 == 0 ? 1 : 0; i < P.n_local; ++i) {
+        const double v = scmwu::np_range_term(&h->X[i * d], ses ? h->v1.data() : nullptr, d,
+                                              h->g1, ses ? h->radii[i] : 0.0, ses);
+        best = v > best || v != v ? v : best;
+    }
+    *D_out = best;
     return SC_OK;
 }
 
