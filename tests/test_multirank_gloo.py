@@ -55,7 +55,8 @@ def _worker(rank, world, port, kind, args, eps, out_path):
         rep, sol = ses.solve_ses(inst, eps, device=dev)
         res = {"radius": sol.radius, "center": list(sol.center), "iters": rep.total_iterations,
                "steps": rep.search_steps, "term": rep.termination.value,
-               "slack": sol.enclosure_slack, "n_local": dev.handle.prob.n_local}
+               "slack": sol.enclosure_slack, "n_local": dev.handle.prob.n_local,
+               "D": dev.handle.prob.D, "D_host": ses.ses_range(inst)[0]}
     else:
         inst, _ = instances.gen_svm(*args)
         dev = shard.svm_device_sharded(inst, comm, engine=eng)
@@ -63,7 +64,8 @@ def _worker(rank, world, port, kind, args, eps, out_path):
         res = {"margin": sol.margin, "pd": sol.pd_distance, "iters": rep.total_iterations,
                "steps": rep.search_steps, "term": rep.termination.value,
                "mu_sum": float(sol.pd_point[0].sum()), "n_mu": len(sol.pd_point[0]),
-               "n_local": dev.handle.prob.n_local}
+               "n_local": dev.handle.prob.n_local,
+               "D": dev.handle.prob.D, "D_host": inst.max_norm}
     with open(f"{out_path}.{rank}", "w") as fh:
         json.dump(res, fh)
     dist.barrier()
@@ -115,6 +117,8 @@ def test_svm_sharded_solve_matches_single(tmp_path, emu_engine):
         assert r["pd"] == pytest.approx(sol.pd_distance, rel=1e-12)
         assert r["n_mu"] == inst.n1 and r["mu_sum"] == pytest.approx(1.0, rel=1e-12)
     assert res[0]["n_local"] + res[1]["n_local"] == inst.n1 + inst.n2
+    # the range from the shards' rows, max-reduced: bit-identical to the host expression
+    assert all(r["D"] == r["D_host"] == inst.max_norm for r in res)
 
 
 def test_ses_sharded_matches_single(tmp_path, emu_engine):
@@ -128,3 +132,5 @@ def test_ses_sharded_matches_single(tmp_path, emu_engine):
     assert r["term"] == rep.termination.value
     assert abs(r["slack"]) <= 1e-9 * r["radius"]
     assert r["radius"] == pytest.approx(sol.radius, rel=2e-3)   # SES: within the spread
+    # the range from the shards' rows (rank 1 has no anchor row: v1, g1 from set_globals)
+    assert r["D"] == r["D_host"] == ses.ses_range(inst)[0]
