@@ -2,7 +2,7 @@
 arguments and outcome, so each call can be replayed on the oracle (the reference's
 algorithm on the CPU) with identical inputs.
 
-    SCMWU_HOST_SEARCH=1 python tools/record_calls.py ses 10000 out.json
+    SCMWU_HOST_SEARCH=1 python tools/record_calls.py ses 10000 out.json [d seed dist]
 """
 import json
 import math
@@ -24,6 +24,9 @@ def _f(x):
 
 def main():
     kind, n, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    d = int(sys.argv[4]) if len(sys.argv) > 4 else 100
+    seed = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+    dist = sys.argv[6] if len(sys.argv) > 6 else "uniform-ball"
     calls = []
     orig_ftp, orig_ref = meta.solve_ftp, meta.refine_run
 
@@ -55,14 +58,14 @@ def main():
 
     meta.solve_ftp, meta.refine_run = ftp, ref
     if kind == "ses":
-        inst = instances.gen_ses(n, 100, 0, "uniform-ball")
+        inst = instances.gen_ses(n, d, seed, dist)
         rep, sol = ses.solve_ses(inst, 1e-3)
         val = sol.radius
     else:
         inst, _ = instances.gen_svm(n // 2, n - n // 2, 100, 0, 1.0)
         rep, sol = svm.solve_svm(inst, 1e-3)
         val = sol.margin
-    json.dump({"kind": kind, "n": n, "iterations": rep.total_iterations,
+    json.dump({"kind": kind, "n": n, "d": d, "seed": seed, "dist": dist, "iterations": rep.total_iterations,
                "value": val, "lower": rep.primal_value, "calls": calls}, open(out, "w"),
               indent=1)
     print(kind, n, rep.total_iterations, val, len(calls))

@@ -26,11 +26,12 @@ def main():
     b = int(sys.argv[3]) if len(sys.argv) > 3 else len(rec["calls"])
     n = rec["n"]
     if rec["kind"] == "ses":
-        inst = instances.gen_ses(n, 100, 0, "uniform-ball")
+        inst = instances.gen_ses(n, rec.get("d", 100), rec.get("seed", 0),
+                                 rec.get("dist", "uniform-ball"))
         pr = O.SesProblem(inst.centers, inst.radii)
         D, _, _ = pr.range()
         spec = pr.spec(3.0 * D / math.sqrt(2.0))
-        d = 100
+        d = rec.get("d", 100)
     else:
         inst, _ = instances.gen_svm(n // 2, n - n // 2, 100, 0, 1.0)
         pr = O.SvmProblem(inst.P, inst.Q)
